@@ -1,0 +1,169 @@
+/*
+ * flycoo.h -- C ABI of the B200 FLYCOO all-mode spMTTKRP + dynamic-remap path.
+ *
+ * Every entry point is plain C: device pointers, host arrays of device
+ * pointers, sizes and a cudaStream_t passed as void*.  No torch types.  All
+ * calls are stream-ordered, allocate nothing (the caller passes workspace)
+ * and return 0 on success or a negative FC_ERR_* code; fc_last_error()
+ * describes the last failure.  Device-detected layout violations are
+ * reported through a caller-provided device flag word (see FC_FLAG_*), which
+ * the host shim turns into the reference's exceptions.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/modecycle):
+ *   fc_mode_worker      <- _kernels.mode_worker            _kernels.py:38-88
+ *                          fanned out by engine.mttkrp_mode engine.py:302-333
+ *   fc_remap_cursor     <- _kernels.mode_worker cursor path _kernels.py:73-82
+ *                          (+ _atomic_fetch_add             _kernels.py:18-35)
+ *   fc_build_*          <- layout.build_sharded             layout.py:462-531
+ *                          + morton.interleave              morton.py:20-44
+ *   fc_synth_*          <- coo.synth_tensor (measurement inputs only;
+ *                          bounded Zipf, not the reference's power law)
+ *                                                           coo.py:323-399
+ */
+#ifndef FLYCOO_H_
+#define FLYCOO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_OK 0
+#define FC_ERR_ARG (-1)          /* bad argument (null pointer, size)       */
+#define FC_ERR_UNSUPPORTED (-2)  /* shape outside what the kernels handle   */
+#define FC_ERR_CUDA (-3)         /* a CUDA launch / runtime call failed     */
+
+/* Bits of the device flag word (int32) written by fc_mode_worker /
+ * fc_remap_cursor.  The host shim raises ShardOverflowError for
+ * FC_FLAG_SLOT_RANGE / FC_FLAG_SHARD_OVERFLOW and BufferOrderError for
+ * FC_FLAG_ROW_OUTSIDE_SS (engine.py:129-134, 343-351). */
+#define FC_FLAG_SLOT_RANGE 1      /* a destination slot >= nnz              */
+#define FC_FLAG_ROW_OUTSIDE_SS 2  /* element's output row not in its chunk's
+                                     super-shard: buffer not ordered for mode */
+#define FC_FLAG_SHARD_OVERFLOW 4  /* cursor strategy: shard fill exceeded   */
+
+/* Element record layout in HBM ("crd" words are int32, 16-B aligned rows):
+ *   N <= 3 : 4 words  {c0, c1, c2, bits(value)}   (N = 2: word 2 is 0)
+ *   N == 4 : 4 words  {c0..c3} + separate float value array
+ *   5..7   : 8 words  {c0..c_{N-1}, 0.., bits(value) in word 7}
+ *   N == 8 : 8 words  {c0..c7} + separate float value array            */
+int fc_crd_words(int nmodes);        /* 4 or 8; <0 when N unsupported   */
+int fc_value_embedded(int nmodes);   /* 1 if the value lives in word CW-1 */
+
+/* Library introspection. */
+int fc_version(void);
+const char *fc_last_error(void);
+/* Largest super-shard row count whose rank-R accumulator tile is kept in
+ * shared memory; larger intervals accumulate in global memory (out rows). */
+int64_t fc_smem_acc_rows_max(int rank);
+int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
+
+/* ------------------------------------------------------------------ K1/K2
+ * One mode pass: for every element i of the active buffer (ordered for
+ * `mode`), y[c_mode,:] += v * prod_{w != mode} F_w[c_w,:] and, if do_remap,
+ * dst[dest_slots[i]] = src[i].
+ *
+ * Work plan (host-built, static per tensor and mode; see engine.py):
+ *   chunk c covers elements [chunk_start[c], chunk_start[c+1]) of one
+ *   super-shard chunk_ss[c]; chunk_part[c] == -1 means the chunk is the only
+ *   one of its super-shard and owns its output rows, otherwise it writes its
+ *   partial rows to part_ws slot chunk_part[c] (rows m_mode x rank floats).
+ *   red_ss[j] / red_part_off[j..j+1] list the super-shards whose rows are
+ *   produced by the deterministic partial reduce (>= 2 partials) or zeroed
+ *   (0 partials).  acc_in_smem must be 1 iff m_mode <=
+ *   fc_smem_acc_rows_max(rank); with acc_in_smem == 0 every chunk must own
+ *   its super-shard and `out` must be zero on entry.
+ * counters[0] += elements processed (the engine.py:335-338 check).        */
+int fc_mode_worker(const void *src_crd, const float *src_val,
+                   void *dst_crd, float *dst_val,
+                   const float *const *factors, /* host array, N device ptrs */
+                   float *out, int nmodes, int mode, int rank,
+                   int64_t out_rows, int64_t m_mode,
+                   const int64_t *chunk_start, const int32_t *chunk_ss,
+                   const int32_t *chunk_part, int64_t nchunks,
+                   const int32_t *red_ss, const int64_t *red_part_off, int64_t nred,
+                   float *part_ws, const uint32_t *dest_slots, int64_t nnz,
+                   int do_compute, int do_remap, int acc_in_smem,
+                   int32_t *flags, unsigned long long *counters, void *stream);
+
+/* Cursor remap strategy (_kernels.py:73-80): b = src_sid[i, next_mode];
+ * slot = dest_base[b] + fetch_add(cursors[b]); dst[slot] = src[i] together
+ * with the element's N shard ids (the reference carries sids in every
+ * element, layout.py:395).  Order inside a shard is nondeterministic;
+ * cursors must be zero on entry. */
+int fc_remap_cursor(const void *src_crd, const float *src_val, void *dst_crd,
+                    float *dst_val, const uint32_t *src_sid, uint32_t *dst_sid,
+                    int nmodes, int next_mode, int64_t nnz, const int64_t *dest_base,
+                    unsigned long long *cursors, int32_t *flags, void *stream);
+
+/* ---------------------------------------------------------------- K5 build
+ * Layout build (layout.py:462-531) in device passes; the host shim
+ * (paper_2309_09131_b200/layout.py) sequences them.  `coords` is (nnz, N)
+ * int32 in input order (seq), `ids` / `keys` are scratch of nnz entries. */
+/* Morton (hi, lo) of interval coordinates iv_w = coords[:, w] / m[w]
+ * (morton.py:20-44); m/k are host arrays.  Returns FC_ERR_UNSUPPORTED if
+ * the key needs more than 128 bits. */
+int fc_build_morton(const int32_t *coords, int64_t nnz, int nmodes,
+                    const int64_t *m, const int64_t *k,
+                    uint64_t *hi, uint64_t *lo, void *stream);
+/* Temp-storage bytes for fc_build_sort_pairs on nnz items. */
+int64_t fc_build_sort_temp_bytes(int64_t nnz);
+/* Stable LSD radix sort of (key, id) pairs on bits [0, end_bit); keys_out /
+ * ids_out receive the sorted sequence. */
+int fc_build_sort_pairs(const uint64_t *keys_in, uint64_t *keys_out,
+                        const uint32_t *ids_in, uint32_t *ids_out, int64_t nnz,
+                        int end_bit, void *temp, int64_t temp_bytes, void *stream);
+/* keys[p] = f(ids[p]) for the sort passes of one mode's canonical order:
+ *   what = 0: lo[id];  1: hi[id];  2: iv_mode[id] = coords[id, mode] / m
+ *   what = 3: (iv_mode[id] << shift) | lo[id]   (single-pass key)        */
+int fc_build_gather_key(const uint32_t *ids, int64_t nnz, int what,
+                        const uint64_t *hi, const uint64_t *lo,
+                        const int32_t *coords, int nmodes, int mode, int64_t m,
+                        int shift, uint64_t *keys, void *stream);
+/* Histogram of iv_mode over k bins (super-shard fills, layout.py:487). */
+int fc_build_ss_hist(const int32_t *coords, int64_t nnz, int nmodes, int mode,
+                     int64_t m, int64_t k, unsigned long long *hist, void *stream);
+/* From the canonical order of one mode: sid[id] = first[iv] + (p - offs[iv]) / g
+ * (layout.py:491-492).  first/offs are device arrays of k+1 int64. */
+int fc_build_shard_ids(const uint32_t *order, int64_t nnz, const int32_t *coords,
+                       int nmodes, int mode, int64_t m, const int64_t *ss_offs,
+                       const int64_t *ss_first, int64_t g, uint32_t *sid, void *stream);
+/* keys[p] = (sid_mode[ids[p]] << 32) | sid_prev[ids[p]]: the B200 intra-shard
+ * order key (Layout). */
+int fc_build_device_key(const uint32_t *ids, int64_t nnz, const uint32_t *sid_mode,
+                        const uint32_t *sid_prev, uint64_t *keys, void *stream);
+/* pos[order[p]] = p */
+int fc_build_invert(const uint32_t *order, int64_t nnz, uint32_t *pos, void *stream);
+/* slot[p] = pos_next[order[p]]  (layout.py:516-519 slot maps) */
+int fc_build_slots(const uint32_t *order, const uint32_t *pos_next, int64_t nnz,
+                   uint32_t *slot, void *stream);
+/* Records of the active buffer in `order`: crd/val per the record layout. */
+int fc_build_records(const uint32_t *order, int64_t nnz, int nmodes,
+                     const int32_t *coords, const float *vals, void *crd,
+                     float *val_out, void *stream);
+
+/* ---------------------------------------------------------------- K6 synth
+ * Measurement-input generator (bench / tests; not the product path).
+ * Draw j, mode w: u = philox(seed, w, j) in [0,1); index = smallest i with
+ * u < cdf_w[i] (bounded Zipf inverse CDF, cdf_w has dims[w] entries ending
+ * in 1.0), or floor(u * dims[w]) when cdf_w is NULL (uniform). */
+int fc_synth_draw(uint64_t seed, int64_t ndraws, int nmodes, const int64_t *dims,
+                  const double *const *cdfs, const int64_t *cdf_len,
+                  int32_t *coords, void *stream);
+/* Linearised keys (mixed radix over dims, 128-bit as hi/lo) of drawn coords. */
+int fc_synth_keys(const int32_t *coords, int64_t n, int nmodes, const int64_t *dims,
+                  uint64_t *hi, uint64_t *lo, void *stream);
+/* keep[ids[p]] = (p == 0 || keys differ from p-1) over a key-sorted run. */
+int fc_synth_mark_first(const uint64_t *hi_sorted, const uint64_t *lo_sorted,
+                        const uint32_t *ids_sorted, int64_t n, uint8_t *keep,
+                        void *stream);
+/* fp32 values in (0, 1]: vals[i] = philox(seed, stream, i). */
+int fc_synth_uniform(uint64_t seed, uint32_t stream_id, int64_t n, float *out,
+                     int open_low, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLYCOO_H_ */

@@ -89,44 +89,59 @@ typedef struct {
   int64_t processed;
 } orc_worker_t;
 
-/* _kernels.py:38-88, statement for statement. */
+/* _kernels.py:38-88, statement for statement (fields hoisted into locals so
+ * the compiler can keep them in registers across the element loop). */
 static void *orc_worker_run(void *arg) {
   orc_worker_t *a = (orc_worker_t *)arg;
   const int64_t R = a->rank, N = a->nmodes;
-  double *ell = (double *)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1));
+  const int mode = a->mode, next_mode = a->next_mode;
+  const int64_t *restrict sids = a->sids;
+  const int64_t *restrict idxs = a->idxs;
+  const double *restrict vals = a->vals;
+  int64_t *restrict dst_sids = a->dst_sids;
+  int64_t *restrict dst_idxs = a->dst_idxs;
+  double *restrict dst_vals = a->dst_vals;
+  const double *restrict fstack = a->fstack;
+  const int64_t *restrict foffs = a->foffs;
+  double *restrict out = a->out;
+  const int64_t *restrict dest_slots = a->dest_slots;
+  const int64_t *restrict dest_base = a->dest_base;
+  const int use_cursor = a->use_cursor, do_compute = a->do_compute, do_remap = a->do_remap;
+  double *restrict ell = (double *)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1));
   int64_t processed = 0;
   for (int64_t s = 0; s < a->nranges; ++s) {
-    for (int64_t i = a->starts[s]; i < a->ends[s]; ++i) {
-      if (a->do_compute) {
+    const int64_t e0 = a->starts[s], e1 = a->ends[s];
+    for (int64_t i = e0; i < e1; ++i) {
+      if (do_compute) {
         for (int64_t r = 0; r < R; ++r) ell[r] = 1.0;
         for (int64_t w = 0; w < N; ++w) {
-          if (w == a->mode) continue;
-          const double *row = a->fstack + (a->foffs[w] + a->idxs[i * N + w]) * R;
+          if (w == mode) continue;
+          const double *restrict row = fstack + (foffs[w] + idxs[i * N + w]) * R;
           for (int64_t r = 0; r < R; ++r) ell[r] *= row[r];
         }
-        const double v = a->vals[i];
-        double *orow = a->out + a->idxs[i * N + a->mode] * R;
+        const double v = vals[i];
+        double *restrict orow = out + idxs[i * N + mode] * R;
         for (int64_t r = 0; r < R; ++r) orow[r] += v * ell[r];
       }
-      if (a->do_remap) {
+      if (do_remap) {
         int64_t slot;
-        if (a->use_cursor) {
-          const int64_t b = a->sids[i * N + a->next_mode];
-          slot = a->dest_base[b] + atomic_fetch_add_explicit(&a->cursors[b], 1,
-                                                             memory_order_relaxed);
-          if (slot >= a->dest_base[b + 1]) {
+        if (use_cursor) {
+          const int64_t b = sids[i * N + next_mode];
+          slot = dest_base[b] + atomic_fetch_add_explicit(&a->cursors[b], 1,
+                                                          memory_order_relaxed);
+          if (slot >= dest_base[b + 1]) {
             atomic_store(a->errflag, b + 1);
             processed += 1;
             continue;
           }
         } else {
-          slot = a->dest_slots[i];
+          slot = dest_slots[i];
         }
         for (int64_t w = 0; w < N; ++w) {
-          a->dst_sids[slot * N + w] = a->sids[i * N + w];
-          a->dst_idxs[slot * N + w] = a->idxs[i * N + w];
+          dst_sids[slot * N + w] = sids[i * N + w];
+          dst_idxs[slot * N + w] = idxs[i * N + w];
         }
-        a->dst_vals[slot] = a->vals[i];
+        dst_vals[slot] = vals[i];
       }
       processed += 1;
     }

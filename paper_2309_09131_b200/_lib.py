@@ -1,0 +1,105 @@
+"""ctypes binding of libflycoo.so (include/flycoo.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every entry point raises.  Build it with ``__graft_entry__.build()``
+(or ``make -C paper_2309_09131_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libflycoo.so"
+
+_c = ctypes
+_vp = _c.c_void_p
+_i64 = _c.c_int64
+_int = _c.c_int
+
+# name -> (restype, argtypes); every pointer is passed as void* (device or
+# host address as an int), sizes as int64.
+_SIGS = {
+    "fc_version": (_int, []),
+    "fc_last_error": (_c.c_char_p, []),
+    "fc_crd_words": (_int, [_int]),
+    "fc_value_embedded": (_int, [_int]),
+    "fc_smem_acc_rows_max": (_i64, [_int]),
+    "fc_tile_elems": (_int, []),
+    "fc_mode_worker": (_int, [
+        _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val
+        _vp, _vp,                      # factors (host array of device ptrs), out
+        _int, _int, _int,              # nmodes, mode, rank
+        _i64, _i64,                    # out_rows, m_mode
+        _vp, _vp, _vp, _i64,           # chunk_start, chunk_ss, chunk_part, nchunks
+        _vp, _vp, _i64,                # red_ss, red_part_off, nred
+        _vp, _vp, _i64,                # part_ws, dest_slots, nnz
+        _int, _int, _int,              # do_compute, do_remap, acc_in_smem
+        _vp, _vp, _vp]),               # flags, counters, stream
+    "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),
+    "fc_build_morton": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fc_build_sort_temp_bytes": (_i64, [_i64]),
+    "fc_build_sort_pairs": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp]),
+    "fc_build_gather_key": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _int, _int, _i64, _int, _vp, _vp]),
+    "fc_build_ss_hist": (_int, [_vp, _i64, _int, _int, _i64, _i64, _vp, _vp]),
+    "fc_build_shard_ids": (_int, [_vp, _i64, _vp, _int, _int, _i64, _vp, _vp, _i64, _vp, _vp]),
+    "fc_build_device_key": (_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
+    "fc_build_invert": (_int, [_vp, _i64, _vp, _vp]),
+    "fc_build_slots": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "fc_build_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fc_synth_draw": (_int, [_c.c_uint64, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fc_synth_keys": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp]),
+    "fc_synth_mark_first": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "fc_synth_uniform": (_int, [_c.c_uint64, _c.c_uint32, _i64, _vp, _int, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class FlycooError(RuntimeError):
+    """A libflycoo entry point returned an error code."""
+
+
+def load():
+    """Load libflycoo.so (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: the CUDA extension was not built "
+                    "(run __graft_entry__.build()); there is no CPU fallback")
+            L = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def call(name: str, *args) -> int:
+    """Call an int-returning entry point; raise FlycooError on failure."""
+    L = load()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        msg = L.fc_last_error().decode(errors="replace")
+        raise FlycooError(f"{name} failed ({rc}): {msg}")
+    return rc
+
+
+def ptr_array(ptrs) -> ctypes.Array:
+    """Host array of device pointers (const float *const *)."""
+    arr = (ctypes.c_void_p * len(ptrs))(*[p if p else None for p in ptrs])
+    return arr
+
+
+def i64_array(vals) -> ctypes.Array:
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])

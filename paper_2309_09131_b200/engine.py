@@ -1,0 +1,289 @@
+"""Drop-in engine: mttkrp_mode / sweep_all_modes / remap_store on the B200.
+
+Same signatures, preconditions, exceptions and counters as the reference
+engine (/root/reference/pkg/src/modecycle/engine.py:28-381).  The per-thread
+numba kernel and its thread fan-out (engine.py:302-333, _kernels.py:38-88)
+become one stream-ordered call of ``fc_mode_worker`` (libflycoo, sm_100a),
+whose CTAs own super-shard chunks.  There is no CPU path: the CUDA library
+must be present.
+
+Differences a caller can see, each forced by the device:
+* ``st`` is a :class:`~.layout.DeviceShardedTensor`, ``factors`` a
+  :class:`~.factors.DeviceFactorSet` (host FactorSet-likes are converted),
+  outputs are fp32 CUDA tensors of shape (I_mode, R);
+* ``workers`` is validated but the GPU decomposition ignores it, and the
+  ScheduleMap is validated (engine.py:274-277) but its assignment unused;
+* ``sweep_all_modes`` runs every mode back to back on the stream and checks
+  the processed counts and device error flags once at the end (one host
+  sync per sweep instead of one per mode); ``mode_seconds`` gets per-mode
+  CUDA-event times.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .factors import DeviceFactorSet
+from .layout import DeviceShardedTensor
+
+__all__ = ["TrafficCounters", "RemapCursors", "ShardOverflowError", "BufferOrderError",
+           "mttkrp_mode", "sweep_all_modes", "remap_store", "REMAP_STRATEGIES"]
+
+REMAP_STRATEGIES = ("slot", "cursor")
+
+FLAG_SLOT_RANGE = 1
+FLAG_ROW_OUTSIDE_SS = 2
+FLAG_SHARD_OVERFLOW = 4
+
+
+class ShardOverflowError(RuntimeError):
+    """A destination shard received more elements than the plan assigns it."""
+
+
+class BufferOrderError(ValueError):
+    """The active buffer is not ordered for the requested mode/strategy."""
+
+
+@dataclass
+class TrafficCounters:
+    """Model data-volume counters per mode, closed forms of engine.py:137-179
+    (tensor read + rewritten once, N-1 rank-R factor rows gathered and one
+    output row updated per element; factor entries counted at 8 bytes as in
+    the reference model)."""
+
+    tensor_bytes_read: int = 0
+    factor_bytes_read: int = 0
+    output_bytes_written: int = 0
+    remap_bytes_written: int = 0
+
+    def add_mode(self, nnz: int, num_modes: int, rank: int, element_bytes: int,
+                 compute: bool = True, remap: bool = True) -> None:
+        if compute:
+            self.tensor_bytes_read += nnz * element_bytes
+            self.factor_bytes_read += nnz * (num_modes - 1) * rank * 8
+            self.output_bytes_written += nnz * rank * 8
+        if remap:
+            if not compute:
+                self.tensor_bytes_read += nnz * element_bytes
+            self.remap_bytes_written += nnz * element_bytes
+
+    def total_bytes(self) -> int:
+        return (self.tensor_bytes_read + self.factor_bytes_read + self.output_bytes_written
+                + self.remap_bytes_written)
+
+    def remap_ratio(self) -> float:
+        other = self.tensor_bytes_read + self.factor_bytes_read + self.output_bytes_written
+        return self.remap_bytes_written / other if other else 0.0
+
+    def as_dict(self) -> dict:
+        return {"tensor_bytes_read": self.tensor_bytes_read,
+                "factor_bytes_read": self.factor_bytes_read,
+                "output_bytes_written": self.output_bytes_written,
+                "remap_bytes_written": self.remap_bytes_written,
+                "remap_ratio": self.remap_ratio()}
+
+
+@dataclass
+class RemapCursors:
+    """Fill records of the upcoming mode's shards (engine.py:182-209)."""
+
+    base: np.ndarray
+    fills: np.ndarray
+
+    @classmethod
+    def for_mode(cls, st, mode: int) -> "RemapCursors":
+        base = st.plan.shard_offsets[mode]
+        return cls(base=base, fills=np.zeros(base.shape[0] - 1, dtype=np.int64))
+
+    def planned_fill(self, shard: int) -> int:
+        return int(self.base[shard + 1] - self.base[shard])
+
+    def reserve(self, shard: int) -> int:
+        if self.fills[shard] >= self.planned_fill(shard):
+            raise ShardOverflowError(
+                f"shard {shard} already holds its planned {self.planned_fill(shard)} elements")
+        slot = int(self.base[shard] + self.fills[shard])
+        self.fills[shard] += 1
+        return slot
+
+    def complete(self) -> bool:
+        return bool(np.array_equal(self.fills, np.diff(self.base)))
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ensure_sids(st: DeviceShardedTensor) -> None:
+    """Materialise per-element shard ids (the reference's `sids`) for the
+    cursor strategy; afterwards they travel with the elements."""
+    if st._sids is None:
+        sids = torch.from_numpy(st.shard_ids().astype(np.int32)).to(st.device)
+        st._sids = [None, None]
+        st._sids[st.active] = sids.contiguous()
+        st._sids[1 - st.active] = torch.empty_like(sids)
+
+
+def remap_store(element_row: int, next_mode: int, cursors: RemapCursors,
+                st: DeviceShardedTensor) -> int:
+    """Store one active element into its next-mode shard slot; returns the
+    slot (engine.py:212-223, single-element mirror of the kernel remap)."""
+    _ensure_sids(st)
+    a, b = st.active, 1 - st.active
+    shard = int(st._sids[a][element_row, next_mode])
+    slot = cursors.reserve(shard)
+    st.crd[b][slot] = st.crd[a][element_row]
+    if st.val[a] is not None:
+        st.val[b][slot] = st.val[a][element_row]
+    st._sids[b][slot] = st._sids[a][element_row]
+    return slot
+
+
+def _coerce_factors(factors, device) -> DeviceFactorSet:
+    if isinstance(factors, DeviceFactorSet):
+        return factors
+    # a reference FactorSet (numpy float64) or any object with .factors
+    fs = getattr(factors, "factors", factors)
+    lam = getattr(factors, "lambdas", None)
+    return DeviceFactorSet(tuple(np.asarray(f, dtype=np.float32) if isinstance(f, np.ndarray) else f
+                                 for f in fs), lam, device)
+
+
+def check_errors(st: DeviceShardedTensor, next_mode: int | None = None) -> None:
+    """Host check of the deferred device counters (engine.py:335-351)."""
+    stat = st._stat.cpu()
+    processed = int(stat[0])
+    flags = int(stat[1]) & 0xFFFFFFFF
+    expected = st._expected
+    st.reset_checks()
+    if flags & FLAG_ROW_OUTSIDE_SS:
+        raise BufferOrderError("an element's output row lies outside its super-shard: the active "
+                               "buffer is not ordered for this mode")
+    if flags & (FLAG_SLOT_RANGE | FLAG_SHARD_OVERFLOW):
+        where = f" of mode {next_mode}" if next_mode is not None else ""
+        raise ShardOverflowError(f"a destination shard{where} overflowed its planned fill")
+    if processed != expected:
+        raise RuntimeError(f"workers processed {processed} of {expected} elements")
+
+
+def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int | None = None,
+                remap: str = "slot", counters: TrafficCounters | None = None,
+                split_remap: bool = False, alloc_log: dict | None = None, *,
+                check: bool = True) -> torch.Tensor:
+    """Output factor for `mode`; leaves the tensor ordered for mode
+    (mode + 1) % N (engine.py:251-354).  For a fixed active order the result
+    is bitwise reproducible (fixed-order sums, no data atomics)."""
+    plan, params = st.plan, st.params
+    nmodes = st.num_modes
+    if not 0 <= mode < nmodes:
+        raise ValueError(f"mode {mode} out of range")
+    if st.active_mode != mode:
+        raise BufferOrderError(f"active buffer is ordered for mode {st.active_mode}, not {mode}")
+    if smap.plan_signature != plan.signature():
+        raise ValueError("schedule was built for a different plan")
+    if smap.num_modes != nmodes:
+        raise ValueError("schedule does not cover this tensor's modes")
+    if remap not in REMAP_STRATEGIES:
+        raise ValueError(f"unknown remap strategy {remap!r}")
+    if remap == "slot" and not st.canonical:
+        raise BufferOrderError(
+            "deterministic-slot remap needs the canonical build order; this tensor was last "
+            "remapped with the cursor strategy")
+    factors = _coerce_factors(factors, st.device)
+    factors.require_match(params.dims)
+    rank = factors.rank
+    next_mode = (mode + 1) % nmodes
+    workers = smap.nu if workers is None else int(workers)
+    if workers < 1:
+        raise ValueError("need at least one worker")
+
+    L = _lib.load()
+    work = st.mode_work(mode, rank)
+    dims = params.dims
+    out = (torch.empty if work.acc_in_smem else torch.zeros)(
+        (dims[mode], rank), dtype=torch.float32, device=st.device)
+    if alloc_log is not None:
+        alloc_log.clear()
+        alloc_log.update({
+            "output_factor": out.numel() * 4,
+            "partial_tiles": 0 if work.part_ws is None else work.part_ws.numel() * 4,
+            "chunk_plan": int(work.chunk_start.numel() * 8 + work.chunk_ss.numel() * 4
+                              + work.chunk_part.numel() * 4),
+        })
+    a, b = st.active, 1 - st.active
+    fptrs = _lib.ptr_array([f.data_ptr() for f in factors.factors])
+    flags_p, proc_p = st.stat_ptrs()
+    strm = _stream()
+    use_cursor = remap == "cursor"
+    if use_cursor:
+        _ensure_sids(st)
+    ref_passes = [(True, True)] if not split_remap else [(True, False), (False, True)]
+    if counters is not None:
+        for c, r in ref_passes:
+            counters.add_mode(st.nnz, nmodes, rank, st.element_nbytes, compute=c, remap=r)
+    # the cursor strategy remaps in its own kernel after the compute pass
+    passes = [(True, False)] if use_cursor else ref_passes
+    val_p = lambda t: t.data_ptr() if t is not None else None
+    for do_compute, do_remap in passes:
+        _lib.call("fc_mode_worker", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
+                  val_p(st.val[b]), fptrs, out.data_ptr(), nmodes, mode, rank, dims[mode],
+                  params.m[mode], work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),
+                  work.chunk_part.data_ptr(), work.nchunks, work.red_ss.data_ptr(),
+                  work.red_part_off.data_ptr(), work.nred,
+                  work.part_ws.data_ptr() if work.part_ws is not None else None,
+                  st.slot_maps[mode].data_ptr(), st.nnz, int(do_compute), int(do_remap),
+                  int(work.acc_in_smem), flags_p, proc_p, strm)
+        st._expected += st.nnz
+    if use_cursor:
+        base = torch.from_numpy(plan.shard_offsets[next_mode]).to(st.device)
+        cursors = torch.zeros(plan.total_shards(next_mode), dtype=torch.int64, device=st.device)
+        _lib.call("fc_remap_cursor", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
+                  val_p(st.val[b]), st._sids[a].data_ptr(), st._sids[b].data_ptr(), nmodes,
+                  next_mode, st.nnz, base.data_ptr(), cursors.data_ptr(), flags_p, strm)
+        if check:
+            check_errors(st, next_mode)
+            want = torch.diff(base)
+            if not torch.equal(cursors, want):
+                bad = int(torch.nonzero(cursors != want)[0, 0])
+                raise ShardOverflowError(
+                    f"destination shard {bad} of mode {next_mode} ended at fill "
+                    f"{int(cursors[bad])}, planned {int(want[bad])}")
+    elif check:
+        check_errors(st, next_mode)
+    st.swap(next_mode, still_canonical=not use_cursor)
+    return out
+
+
+def sweep_all_modes(st: DeviceShardedTensor, factors, smap, workers: int | None = None,
+                    remap: str = "slot", counters: TrafficCounters | None = None,
+                    mode_seconds: list | None = None, split_remap: bool = False) -> DeviceFactorSet:
+    """One pass over every mode, each factor overwritten by its raw MTTKRP
+    output right after its mode (engine.py:357-381)."""
+    factors = _coerce_factors(factors, st.device)
+    working = list(factors.factors)
+    lambdas = factors.lambdas.copy()
+    events = []
+    for n in range(st.num_modes):
+        current = DeviceFactorSet(tuple(working), lambdas, st.device, validate=False)
+        if mode_seconds is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        # cursor passes verify cursor fills per mode (needs a sync); slot
+        # passes defer their device checks to the end of the sweep
+        working[n] = mttkrp_mode(st, current, n, smap, workers=workers, remap=remap,
+                                 counters=counters, split_remap=split_remap,
+                                 check=(remap == "cursor"))
+        if mode_seconds is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            events.append((e0, e1))
+    if remap != "cursor":
+        check_errors(st)
+    if mode_seconds is not None:
+        torch.cuda.current_stream().synchronize()
+        mode_seconds.extend(e0.elapsed_time(e1) / 1e3 for e0, e1 in events)
+    return DeviceFactorSet(tuple(working), lambdas, st.device, validate=False)

@@ -1,0 +1,400 @@
+"""The FLYCOO layout in HBM: plan, double-buffered element records, slot maps.
+
+Mirrors the reference's data model (/root/reference/pkg/src/modecycle/
+layout.py:344-531) with a B200 memory layout:
+
+* records: int32 coordinates + fp32 value, 16 B per element for N <= 3
+  (value in word 3), 20 B for N = 4 (value array beside the 16-B coordinate
+  rows) -- see include/flycoo.h; two buffers (ping-pong) of nnz records;
+* slot maps: one uint32 per element per mode, ``slot[n][i]`` = position in
+  the mode-(n+1) buffer of the element at mode-n position i
+  (layout.py:516-519);
+* plan arrays (super-shard fills, shard offsets) on the host, identical to
+  the reference's.
+
+Element order: the reference's canonical order fixes shard membership and
+shard offsets (layout.py:484-497) and this build keeps both bit-exactly.
+Inside each shard the order is free (the reference checks shards only at
+shard granularity, layout.py:615-625); this build orders a shard's elements
+by (previous-mode shard id, Morton key, input position), so every remap
+writes each (source shard -> destination shard) group as one contiguous run
+(DESIGN.md "Layout").
+
+:func:`build_device_sharded` runs the build on the GPU through the K5
+entry points of libflycoo (radix sorts, histograms, scatters).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .params import PartitionParams
+
+__all__ = ["PartitionPlan", "DeviceShardedTensor", "build_device_sharded", "plan_from_counts",
+           "record_bytes", "ModeWork"]
+
+
+def record_bytes(nmodes: int) -> int:
+    """Logical bytes of one element record (int32 coords + fp32 value)."""
+    return 4 * nmodes + 4
+
+
+def _cdiv(a, b):
+    return -(-a // b)
+
+
+@dataclass(frozen=True, eq=False)
+class PartitionPlan:
+    """Per-mode geometry (layout.py:344-381): super-shard fills and prefix
+    sums, shard counts, and every shard's element offset."""
+
+    params: PartitionParams
+    ss_counts: tuple
+    ss_elem_offsets: tuple
+    ss_shard_counts: tuple
+    ss_first_shard: tuple
+    shard_offsets: tuple
+
+    @property
+    def num_modes(self) -> int:
+        return self.params.num_modes
+
+    @property
+    def nnz(self) -> int:
+        return self.params.nnz
+
+    def total_shards(self, mode: int) -> int:
+        return int(self.ss_first_shard[mode][-1])
+
+    def shard_fills(self, mode: int) -> np.ndarray:
+        return np.diff(self.shard_offsets[mode])
+
+    def ss_of_shard(self, mode: int) -> np.ndarray:
+        return np.repeat(np.arange(self.params.k[mode], dtype=np.int64), self.ss_shard_counts[mode])
+
+    def signature(self) -> tuple:
+        return (self.params.dims, self.params.nnz, self.params.m, self.params.g)
+
+    def pointer_entries(self) -> int:
+        return sum(self.total_shards(n) for n in range(self.num_modes))
+
+
+def plan_from_counts(params: PartitionParams, counts_per_mode) -> PartitionPlan:
+    """Shard geometry from super-shard fills (layout.py:487-497)."""
+    g, nnz = params.g, params.nnz
+    cols = {k: [] for k in ("c", "o", "s", "f", "so")}
+    for n, counts in enumerate(counts_per_mode):
+        counts = np.asarray(counts, dtype=np.int64)
+        offs = np.concatenate(([0], np.cumsum(counts))).astype(np.int64)
+        shards = -(-counts // g)
+        first = np.concatenate(([0], np.cumsum(shards))).astype(np.int64)
+        ss_of = np.repeat(np.arange(params.k[n], dtype=np.int64), shards)
+        q = np.arange(int(first[-1]), dtype=np.int64) - first[ss_of]
+        soffs = np.concatenate((offs[ss_of] + q * g, [nnz])).astype(np.int64)
+        for key, arr in zip(("c", "o", "s", "f", "so"), (counts, offs, shards, first, soffs)):
+            cols[key].append(arr)
+    return PartitionPlan(params, tuple(cols["c"]), tuple(cols["o"]), tuple(cols["s"]),
+                         tuple(cols["f"]), tuple(cols["so"]))
+
+
+@dataclass
+class ModeWork:
+    """Static CTA work plan of one mode (see fc_mode_worker in flycoo.h)."""
+    acc_in_smem: bool
+    nchunks: int
+    chunk_start: torch.Tensor   # int64 (nchunks + 1)
+    chunk_ss: torch.Tensor      # int32
+    chunk_part: torch.Tensor    # int32
+    nred: int
+    red_ss: torch.Tensor        # int32
+    red_part_off: torch.Tensor  # int64 (nred + 1)
+    nparts: int
+    part_ws: torch.Tensor | None
+    chunk_elems: int
+
+
+def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None) -> ModeWork:
+    """Split every super-shard of `mode` into CTA chunks.  Shared-memory
+    accumulation (m rows fit): chunks of `chunk_elems`, super-shards with
+    several chunks get one partial tile per chunk, summed in chunk order by
+    K2.  Otherwise one chunk per super-shard accumulating in `out`."""
+    L = _lib.load()
+    params = plan.params
+    m = int(params.m[mode])
+    counts = np.asarray(plan.ss_counts[mode], dtype=np.int64)
+    offs = np.asarray(plan.ss_elem_offsets[mode], dtype=np.int64)
+    k = counts.shape[0]
+    nnz = plan.nnz
+    tile = int(L.fc_tile_elems())
+    smem = m <= int(L.fc_smem_acc_rows_max(int(rank)))
+    if smem:
+        if chunk_elems is None:
+            want = _cdiv(max(nnz, 1), 148 * 4)
+            chunk_elems = int(min(8192, max(tile, _cdiv(want, tile) * tile)))
+        C = int(chunk_elems)
+        nch = -(-counts // C)
+    else:
+        C = 0
+        nch = (counts > 0).astype(np.int64)
+    total = int(nch.sum())
+    ss_of = np.repeat(np.arange(k, dtype=np.int64), nch)
+    first_chunk = np.concatenate(([0], np.cumsum(nch)))[:-1]
+    j = np.arange(total, dtype=np.int64) - first_chunk[ss_of]
+    starts = offs[ss_of] + (j * C if smem else 0)
+    chunk_start = np.concatenate((starts, [nnz])).astype(np.int64)
+    if smem:
+        multi = nch >= 2
+        part_base = np.concatenate(([0], np.cumsum(np.where(multi, nch, 0))))
+        part = np.where(multi[ss_of], part_base[:-1][ss_of] + j, -1).astype(np.int32)
+        red_mask = (nch == 0) | multi
+        red_ss = np.nonzero(red_mask)[0].astype(np.int32)
+        # partial ranges are contiguous in super-shard order, so entry j's
+        # range ends where entry j+1's begins (single-chunk ones add none)
+        red_off = np.concatenate((part_base[:-1][red_mask], [part_base[-1]])).astype(np.int64)
+        nparts = int(part_base[-1])
+    else:
+        part = np.full(total, -1, dtype=np.int32)
+        red_ss = np.zeros(0, dtype=np.int32)
+        red_off = np.zeros(1, dtype=np.int64)
+        nparts = 0
+    dev = torch.device(device)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ws = torch.empty(max(nparts, 1) * m * rank, dtype=torch.float32, device=dev) if nparts else None
+    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), int(red_ss.size),
+                    t(red_ss), t(red_off), nparts, ws, C)
+
+
+class DeviceShardedTensor:
+    """Double-buffered FLYCOO tensor resident in HBM (the reference's
+    ShardedTensor, layout.py:384-459, with device buffers)."""
+
+    def __init__(self, plan: PartitionPlan, crd, val, slot_maps, device):
+        self.plan = plan
+        self.crd = crd              # [2] int32 (nnz, CW)
+        self.val = val              # [2] float32 (nnz,) or [None, None]
+        self.slot_maps = slot_maps  # per mode int32 (uint32 bits) (nnz,)
+        self.device = torch.device(device)
+        self.active = 0
+        self.active_mode = 0
+        self.canonical = True
+        self._work = {}
+        # [processed elements, error flags] for the deferred end-of-pass checks
+        self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self._expected = 0
+        self._sids = None           # per-element shard ids, only for the cursor strategy
+
+    # --------------------------------------------------------------- props
+    @property
+    def params(self) -> PartitionParams:
+        return self.plan.params
+
+    @property
+    def nnz(self) -> int:
+        return self.plan.nnz
+
+    @property
+    def num_modes(self) -> int:
+        return self.plan.num_modes
+
+    @property
+    def element_nbytes(self) -> int:
+        return record_bytes(self.num_modes)
+
+    def swap(self, new_mode: int, still_canonical: bool) -> None:
+        self.active = 1 - self.active
+        self.active_mode = new_mode
+        self.canonical = self.canonical and still_canonical
+
+    def mode_work(self, mode: int, rank: int) -> ModeWork:
+        key = (mode, rank)
+        if key not in self._work:
+            self._work[key] = make_mode_work(self.plan, mode, rank, self.device)
+        return self._work[key]
+
+    # ----------------------------------------------------- host-side views
+    def device_arrays(self, which: int | None = None):
+        b = self.active if which is None else which
+        return self.crd[b], self.val[b]
+
+    def _host_coords_vals(self, which: int):
+        crd, val = self.crd[which], self.val[which]
+        N = self.num_modes
+        c = crd[:, :N].to(torch.int64).cpu().numpy()
+        if val is None:
+            v = crd[:, -1].view(torch.float32).cpu().numpy().astype(np.float64)
+        else:
+            v = val.cpu().numpy().astype(np.float64)
+        return c, v
+
+    def positions_in_mode(self, mode: int) -> torch.Tensor:
+        """Mode-`mode` buffer position of every element of the active buffer
+        (composition of slot maps; needs the canonical arrangement)."""
+        if not self.canonical:
+            raise ValueError("positions are only defined for the canonical arrangement")
+        N = self.num_modes
+        pos = torch.arange(self.nnz, device=self.device, dtype=torch.int64)
+        n = self.active_mode
+        while n != mode:
+            pos = (self.slot_maps[n].to(torch.int64) & 0xFFFFFFFF)[pos]
+            n = (n + 1) % N
+        return pos
+
+    def shard_ids(self) -> np.ndarray:
+        """(nnz, N) int64 shard id per mode of the active buffer's elements."""
+        if self._sids is not None:
+            return self._sids[self.active].to(torch.int64).cpu().numpy()
+        out = np.empty((self.nnz, self.num_modes), dtype=np.int64)
+        for w in range(self.num_modes):
+            pos = self.positions_in_mode(w).cpu().numpy()
+            out[:, w] = np.searchsorted(self.plan.shard_offsets[w], pos, side="right") - 1
+        return out
+
+    def active_arrays(self):
+        """(sids, idxs, vals) of the active buffer as host numpy arrays in the
+        reference's dtypes (int64, int64, float64) -- a validation view, not
+        the hot path (layout.py:419-421)."""
+        c, v = self._host_coords_vals(self.active)
+        return self.shard_ids(), c, v
+
+    def to_coo(self):
+        c, v = self._host_coords_vals(self.active)
+        return c, v
+
+    def accounting(self) -> dict:
+        plan_aux = sum(a.size for g in (self.plan.ss_counts, self.plan.ss_elem_offsets,
+                                        self.plan.ss_shard_counts, self.plan.ss_first_shard)
+                       for a in g)
+        buf = sum(t.numel() * t.element_size() for t in self.crd)
+        buf += sum(t.numel() * t.element_size() for t in self.val if t is not None)
+        return {
+            "buffer_elements": 2 * self.nnz,
+            "element_bytes": self.element_nbytes,
+            "buffer_bytes": buf,
+            "remap_pointer_entries": self.plan.pointer_entries(),
+            "slot_rank_entries": sum(s.numel() for s in self.slot_maps),
+            "plan_aux_entries": plan_aux,
+        }
+
+    # ------------------------------------------------------ deferred checks
+    def reset_checks(self):
+        self._stat.zero_()
+        self._expected = 0
+
+    def stat_ptrs(self):
+        base = self._stat.data_ptr()
+        return base + 8, base  # (flags int32*, processed u64*)
+
+
+# ------------------------------------------------------------------- build
+
+def _stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _bitlen(x: int) -> int:
+    return int(x).bit_length()
+
+
+def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> DeviceShardedTensor:
+    """Device build of the FLYCOO layout (layout.py:462-531 + the B200
+    intra-shard order).  `subs` (nnz, N) and `vals` (nnz,) in input order,
+    as numpy arrays or torch tensors (any device)."""
+    L = _lib.load()
+    dev = torch.device(device)
+    subs_t = torch.as_tensor(subs)
+    vals_t = torch.as_tensor(vals)
+    nnz, N = int(subs_t.shape[0]), int(subs_t.shape[1])
+    if tuple(params.dims) != tuple(int(d) for d in params.dims) or len(params.dims) != N:
+        raise ValueError("params were selected for different dims")
+    if params.nnz != nnz:
+        raise ValueError("params were selected for a different nonzero count")
+    if nnz >= 1 << 32:
+        raise ValueError("nnz must fit uint32 positions")
+    if max(params.dims) >= 1 << 31:
+        raise ValueError("dims must fit int32 coordinates")
+    coords = subs_t.to(device=dev, dtype=torch.int32).contiguous()
+    fvals = vals_t.to(device=dev, dtype=torch.float32).contiguous()
+    st = _stream_ptr()
+    P = lambda t: t.data_ptr() if t is not None else None
+    m_arr = _lib.i64_array(params.m)
+    k_arr = _lib.i64_array(params.k)
+
+    widths = [_bitlen(k - 1) for k in params.k]
+    W = sum(widths)
+    hi = torch.empty(nnz, dtype=torch.int64, device=dev)
+    lo = torch.empty(nnz, dtype=torch.int64, device=dev)
+    _lib.call("fc_build_morton", P(coords), nnz, N, m_arr, k_arr, P(hi), P(lo), st)
+
+    temp_bytes = int(L.fc_build_sort_temp_bytes(max(nnz, 1)))
+    temp = torch.empty(max(temp_bytes, 1), dtype=torch.uint8, device=dev)
+    keys_a = torch.empty(nnz, dtype=torch.int64, device=dev)
+    keys_b = torch.empty(nnz, dtype=torch.int64, device=dev)
+    iota = torch.arange(nnz, dtype=torch.int32, device=dev)
+
+    def sort_pass(ids, what, end_bit, mode=0, m=1, shift=0):
+        if end_bit <= 0:
+            return ids
+        _lib.call("fc_build_gather_key", P(ids), nnz, what, P(hi), P(lo), P(coords), N, mode, m,
+                  shift, P(keys_a), st)
+        out = torch.empty_like(ids)
+        _lib.call("fc_build_sort_pairs", P(keys_a), P(keys_b), P(ids), P(out), nnz, min(end_bit, 64),
+                  P(temp), temp_bytes, st)
+        return out
+
+    orders, sids, counts_all = [], [], []
+    hist = torch.empty(max(params.k), dtype=torch.int64, device=dev)
+    for n in range(N):
+        B = _bitlen(params.k[n] - 1)
+        if W + B <= 64:
+            order = sort_pass(iota, 3, W + B, n, params.m[n], W)
+        else:
+            order = sort_pass(iota, 0, min(W, 64))
+            if W > 64:
+                order = sort_pass(order, 1, W - 64)
+            order = sort_pass(order, 2, B, n, params.m[n])
+        if order is iota:
+            order = iota.clone()
+        _lib.call("fc_build_ss_hist", P(coords), nnz, N, n, params.m[n], params.k[n], P(hist), st)
+        counts_all.append(hist[: params.k[n]].cpu().numpy().astype(np.int64))
+        orders.append(order)
+    plan = plan_from_counts(params, counts_all)
+    if any(int(c.sum()) != nnz for c in counts_all):
+        raise ValueError("coordinates outside the declared dims")
+    for n in range(N):
+        offs = torch.from_numpy(plan.ss_elem_offsets[n]).to(dev)
+        first = torch.from_numpy(plan.ss_first_shard[n]).to(dev)
+        sid = torch.empty(nnz, dtype=torch.int32, device=dev)
+        _lib.call("fc_build_shard_ids", P(orders[n]), nnz, P(coords), N, n, params.m[n], P(offs),
+                  P(first), params.g, P(sid), st)
+        sids.append(sid)
+    gorders, gpos = [], []
+    for n in range(N):
+        prev = (n - 1) % N
+        end_bit = 32 + _bitlen(plan.total_shards(n) - 1)
+        _lib.call("fc_build_device_key", P(orders[n]), nnz, P(sids[n]), P(sids[prev]), P(keys_a), st)
+        g_ord = torch.empty_like(orders[n])
+        _lib.call("fc_build_sort_pairs", P(keys_a), P(keys_b), P(orders[n]), P(g_ord), nnz,
+                  min(end_bit, 64), P(temp), temp_bytes, st)
+        pos = torch.empty(nnz, dtype=torch.int32, device=dev)
+        _lib.call("fc_build_invert", P(g_ord), nnz, P(pos), st)
+        gorders.append(g_ord)
+        gpos.append(pos)
+    slot_maps = []
+    for n in range(N):
+        slot = torch.empty(nnz, dtype=torch.int32, device=dev)
+        _lib.call("fc_build_slots", P(gorders[n]), P(gpos[(n + 1) % N]), nnz, P(slot), st)
+        slot_maps.append(slot)
+    cw = int(L.fc_crd_words(N))
+    emb = bool(L.fc_value_embedded(N))
+    crd = [torch.empty((nnz, cw), dtype=torch.int32, device=dev),
+           torch.zeros((nnz, cw), dtype=torch.int32, device=dev)]
+    val = [None, None] if emb else [torch.empty(nnz, dtype=torch.float32, device=dev),
+                                    torch.zeros(nnz, dtype=torch.float32, device=dev)]
+    _lib.call("fc_build_records", P(gorders[0]), nnz, N, P(coords), P(fvals), P(crd[0]),
+              P(val[0]), st)
+    torch.cuda.current_stream().synchronize()
+    return DeviceShardedTensor(plan, crd, val, tuple(slot_maps), dev)

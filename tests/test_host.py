@@ -1,0 +1,97 @@
+"""CPU-only checks: generators pinned to the reference, host planning,
+the C-ABI library loads and exports every symbol of include/flycoo.h."""
+import hashlib
+import json
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+from paper_2309_09131_b200 import _lib
+from paper_2309_09131_b200.layout import make_mode_work, plan_from_counts
+from paper_2309_09131_b200.params import device_params, select_params
+from paper_2309_09131_b200.schedule import _lpt
+from paper_2309_09131_b200.synth import synth_tensor, zipf_cdf
+
+
+def test_synth_small_matches_reference():
+    z = np.load(GOLDEN / "synth_small.npz")
+    subs, vals = synth_tensor((50, 40, 30), 3000, seed=5, skew=0.0)
+    assert np.array_equal(subs, z["subs"]) and np.array_equal(vals, z["vals"])
+
+
+@pytest.mark.slow
+def test_synth_c1_matches_reference_digest():
+    d = json.loads((GOLDEN / "synth_c1.json").read_text())
+    subs, vals = synth_tensor((1000, 800, 600), 1_000_000, seed=1, skew=0.0)
+    assert subs[:8].tolist() == d["head_subs"]
+    assert hashlib.sha256(np.ascontiguousarray(subs, dtype="<i8").tobytes()).hexdigest() == d["subs_sha256"]
+    assert hashlib.sha256(np.ascontiguousarray(vals, dtype="<f8").tobytes()).hexdigest() == d["vals_sha256"]
+
+
+def test_zipf_cdf():
+    c = zipf_cdf(10, 1.1)
+    assert c[-1] == 1.0 and np.all(np.diff(c) > 0)
+    p = np.diff(np.concatenate(([0], c)))
+    assert abs(p[0] / p[1] - 2 ** 1.1) < 1e-9
+
+
+def test_schedule_lpt_matches_reference():
+    for case in json.loads((GOLDEN / "schedule.json").read_text()):
+        assert _lpt(case["counts"], case["nu"]) == case["assign"]
+
+
+def test_header_symbols_exported():
+    """Every entry point declared in include/flycoo.h is bound and exported."""
+    hdr = (ROOT / "include" / "flycoo.h").read_text()
+    declared = set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(fc_[a-z_0-9]+)\(", hdr, re.M))
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.exported_symbols())
+    L = _lib.load()
+    for name in declared:
+        assert getattr(L, name) is not None
+    assert L.fc_version() == 1
+    assert L.fc_crd_words(3) == 4 and L.fc_value_embedded(3) == 1
+    assert L.fc_crd_words(4) == 4 and L.fc_value_embedded(4) == 0
+    assert L.fc_crd_words(6) == 8 and L.fc_value_embedded(6) == 1
+    assert L.fc_tile_elems() == 2048
+    assert L.fc_smem_acc_rows_max(32) == 512
+
+
+def test_plan_from_counts_matches_reference_layout():
+    z = dict(np.load(GOLDEN / "layout_n3_skew.npz"))
+    N = len(z["dims"])
+    params = select_params(tuple(z["dims"]), len(z["vals"]), 4, 32 << 20, int(z["rank"]),
+                           g_range=(64, 1024))
+    plan = plan_from_counts(params, [z[f"ss_counts{n}"] for n in range(N)])
+    for n in range(N):
+        assert np.array_equal(plan.shard_offsets[n], z[f"shard_offsets{n}"])
+        assert np.array_equal(plan.ss_first_shard[n], z[f"ss_first_shard{n}"])
+
+
+def test_mode_work_partitions_elements():
+    rng = np.random.default_rng(0)
+    params = device_params((1000, 300, 50), 200_000, 32)
+    counts = [np.bincount(np.minimum(rng.zipf(1.5, 200_000) - 1, d - 1) // params.m[n],
+                          minlength=params.k[n]) for n, d in enumerate(params.dims)]
+    plan = plan_from_counts(params, counts)
+    for n in range(3):
+        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=4096)
+        cs = w.chunk_start.numpy()
+        assert cs[0] == 0 and cs[-1] == plan.nnz and np.all(np.diff(cs) > 0)
+        ss = w.chunk_ss.numpy()
+        offs = plan.ss_elem_offsets[n]
+        # every chunk lies inside its super-shard
+        assert np.all(cs[:-1] >= offs[ss]) and np.all(cs[1:] <= offs[ss + 1])
+        part = w.chunk_part.numpy()
+        nch = np.bincount(ss, minlength=params.k[n])
+        assert np.all((part >= 0) == (nch[ss] >= 2))
+        red = w.red_ss.numpy()
+        assert set(red.tolist()) == set(np.nonzero((nch == 0) | (nch >= 2))[0].tolist())
+        roff = w.red_part_off.numpy()
+        for j, s in enumerate(red):
+            assert roff[j + 1] - roff[j] == (nch[s] if nch[s] >= 2 else 0)
+            got = sorted(part[ss == s].tolist())
+            if nch[s] >= 2:
+                assert got == list(range(roff[j], roff[j + 1]))
