@@ -271,7 +271,7 @@ def run_ours(args, rank, world, local):
     kern_s = sum(mode_secs)
     achieved = sum(per_mode) * args.steps / kern_s / 1e9
     peak, peak_src = peaks()
-    launches_per_step = sum(1 + (1 if st.mode_work(n, R).nred > 0 else 0) for n in range(N))
+    launches_per_step = sum(st.mode_work(n, R).launches for n in range(N))
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
@@ -333,7 +333,7 @@ def run_ours(args, rank, world, local):
                        "mode_ms": [round(1e3 * x, 4) for x in mode_secs[:N]]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "mode_pass_kernel (+ reduce_partials_kernel)",
+                         "kernel": "mode_pass_fast_kernel (+ reduce_level_kernel)",
                          "algorithmic_bytes_per_launch": per_mode[0], "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches_per_step * args.steps,

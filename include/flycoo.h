@@ -65,16 +65,19 @@ int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
  * `mode`), y[c_mode,:] += v * prod_{w != mode} F_w[c_w,:] and, if do_remap,
  * dst[dest_slots[i]] = src[i].
  *
- * Work plan (host-built, static per tensor and mode; see engine.py):
+ * Work plan (host-built, static per tensor and mode; see layout.py):
  *   chunk c covers elements [chunk_start[c], chunk_start[c+1]) of one
  *   super-shard chunk_ss[c]; chunk_part[c] == -1 means the chunk is the only
  *   one of its super-shard and owns its output rows, otherwise it writes its
- *   partial rows to part_ws slot chunk_part[c] (rows m_mode x rank floats).
- *   red_ss[j] / red_part_off[j..j+1] list the super-shards whose rows are
- *   produced by the deterministic partial reduce (>= 2 partials) or zeroed
- *   (0 partials).  acc_in_smem must be 1 iff m_mode <=
- *   fc_smem_acc_rows_max(rank); with acc_in_smem == 0 every chunk must own
- *   its super-shard and `out` must be zero on entry.
+ *   partial rows to part_ws slot chunk_part[c] (m_mode x rank floats).
+ *   Deterministic two-level reduce of the partials (K2): red1 holds nred1
+ *   tasks {ss, p0, p1, dst}: rows of super-shard ss = sum of partials
+ *   [p0, p1) in chunk order, written to `out` (dst < 0) or to part_ws2 slot
+ *   dst; red2 holds nred2 tasks {ss, q0, q1} summing part_ws2 slots [q0, q1)
+ *   into `out`.  Empty super-shards appear as {ss, 0, 0, -1} (zero rows).
+ *   acc_in_smem must be 1 iff m_mode <= fc_smem_acc_rows_max(rank); with
+ *   acc_in_smem == 0 every chunk must own its super-shard and `out` must be
+ *   zero on entry.
  * counters[0] += elements processed (the engine.py:335-338 check).        */
 int fc_mode_worker(const void *src_crd, const float *src_val,
                    void *dst_crd, float *dst_val,
@@ -83,8 +86,8 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
                    int64_t out_rows, int64_t m_mode,
                    const int64_t *chunk_start, const int32_t *chunk_ss,
                    const int32_t *chunk_part, int64_t nchunks,
-                   const int32_t *red_ss, const int64_t *red_part_off, int64_t nred,
-                   float *part_ws, const uint32_t *dest_slots, int64_t nnz,
+                   const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
+                   float *part_ws, float *part_ws2, const uint32_t *dest_slots, int64_t nnz,
                    int do_compute, int do_remap, int acc_in_smem,
                    int32_t *flags, unsigned long long *counters, void *stream);
 

@@ -34,8 +34,8 @@ _SIGS = {
         _int, _int, _int,              # nmodes, mode, rank
         _i64, _i64,                    # out_rows, m_mode
         _vp, _vp, _vp, _i64,           # chunk_start, chunk_ss, chunk_part, nchunks
-        _vp, _vp, _i64,                # red_ss, red_part_off, nred
-        _vp, _vp, _i64,                # part_ws, dest_slots, nnz
+        _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
+        _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots, nnz
         _int, _int, _int,              # do_compute, do_remap, acc_in_smem
         _vp, _vp, _vp]),               # flags, counters, stream
     "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),

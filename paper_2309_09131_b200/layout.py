@@ -109,12 +109,43 @@ class ModeWork:
     chunk_start: torch.Tensor   # int64 (nchunks + 1)
     chunk_ss: torch.Tensor      # int32
     chunk_part: torch.Tensor    # int32
-    nred: int
-    red_ss: torch.Tensor        # int32
-    red_part_off: torch.Tensor  # int64 (nred + 1)
+    red1: torch.Tensor          # int64 (nred1, 4): ss, p0, p1, dst
+    nred1: int
+    red2: torch.Tensor          # int64 (nred2, 3): ss, q0, q1
+    nred2: int
     nparts: int
     part_ws: torch.Tensor | None
+    part_ws2: torch.Tensor | None
     chunk_elems: int
+
+    @property
+    def launches(self) -> int:
+        """Kernels one mode pass launches (K1, plus the K2 levels)."""
+        return 1 + (1 if self.nred1 else 0) + (1 if self.nred2 else 0)
+
+
+REDUCE_FAN = 64  # partials summed per level-1 reduce task
+
+
+def reduce_plan(nch: np.ndarray, part_base: np.ndarray, fan: int = REDUCE_FAN):
+    """Two-level deterministic reduce tasks (fc_mode_worker K2) for the
+    super-shards with 0 or >= 2 chunks."""
+    red1, red2 = [], []
+    slot = 0
+    for ss in np.nonzero((nch == 0) | (nch >= 2))[0]:
+        P = int(nch[ss]) if nch[ss] >= 2 else 0
+        p0 = int(part_base[ss])
+        if P <= fan:
+            red1.append((ss, p0, p0 + P, -1))
+            continue
+        groups = -(-P // fan)
+        for g in range(groups):
+            red1.append((ss, p0 + g * fan, p0 + min(P, (g + 1) * fan), slot + g))
+        red2.append((ss, slot, slot + groups))
+        slot += groups
+    r1 = np.asarray(red1, dtype=np.int64).reshape(-1, 4)
+    r2 = np.asarray(red2, dtype=np.int64).reshape(-1, 3)
+    return r1, r2, slot
 
 
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None) -> ModeWork:
@@ -146,26 +177,23 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
     j = np.arange(total, dtype=np.int64) - first_chunk[ss_of]
     starts = offs[ss_of] + (j * C if smem else 0)
     chunk_start = np.concatenate((starts, [nnz])).astype(np.int64)
+    dev = torch.device(device)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     if smem:
         multi = nch >= 2
         part_base = np.concatenate(([0], np.cumsum(np.where(multi, nch, 0))))
         part = np.where(multi[ss_of], part_base[:-1][ss_of] + j, -1).astype(np.int32)
-        red_mask = (nch == 0) | multi
-        red_ss = np.nonzero(red_mask)[0].astype(np.int32)
-        # partial ranges are contiguous in super-shard order, so entry j's
-        # range ends where entry j+1's begins (single-chunk ones add none)
-        red_off = np.concatenate((part_base[:-1][red_mask], [part_base[-1]])).astype(np.int64)
         nparts = int(part_base[-1])
+        r1, r2, nslots = reduce_plan(nch, part_base)
     else:
         part = np.full(total, -1, dtype=np.int32)
-        red_ss = np.zeros(0, dtype=np.int32)
-        red_off = np.zeros(1, dtype=np.int64)
-        nparts = 0
-    dev = torch.device(device)
-    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    ws = torch.empty(max(nparts, 1) * m * rank, dtype=torch.float32, device=dev) if nparts else None
-    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), int(red_ss.size),
-                    t(red_ss), t(red_off), nparts, ws, C)
+        nparts, nslots = 0, 0
+        r1 = np.zeros((0, 4), dtype=np.int64)
+        r2 = np.zeros((0, 3), dtype=np.int64)
+    ws = torch.empty(nparts * m * rank, dtype=torch.float32, device=dev) if nparts else None
+    ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
+    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part),
+                    t(r1), int(r1.shape[0]), t(r2), int(r2.shape[0]), nparts, ws, ws2, C)
 
 
 class DeviceShardedTensor:

@@ -77,7 +77,7 @@ def test_mode_work_partitions_elements():
                           minlength=params.k[n]) for n, d in enumerate(params.dims)]
     plan = plan_from_counts(params, counts)
     for n in range(3):
-        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=4096)
+        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=2048)
         cs = w.chunk_start.numpy()
         assert cs[0] == 0 and cs[-1] == plan.nnz and np.all(np.diff(cs) > 0)
         ss = w.chunk_ss.numpy()
@@ -87,11 +87,16 @@ def test_mode_work_partitions_elements():
         part = w.chunk_part.numpy()
         nch = np.bincount(ss, minlength=params.k[n])
         assert np.all((part >= 0) == (nch[ss] >= 2))
-        red = w.red_ss.numpy()
-        assert set(red.tolist()) == set(np.nonzero((nch == 0) | (nch >= 2))[0].tolist())
-        roff = w.red_part_off.numpy()
-        for j, s in enumerate(red):
-            assert roff[j + 1] - roff[j] == (nch[s] if nch[s] >= 2 else 0)
-            got = sorted(part[ss == s].tolist())
-            if nch[s] >= 2:
-                assert got == list(range(roff[j], roff[j + 1]))
+        r1 = w.red1.numpy()
+        r2 = w.red2.numpy()
+        red = sorted(set(r1[:, 0].tolist()))
+        assert red == sorted(np.nonzero((nch == 0) | (nch >= 2))[0].tolist())
+        # every partial of a multi-chunk super-shard is summed exactly once
+        for s_ in red:
+            t1 = r1[r1[:, 0] == s_]
+            covered = sorted(q for a_, b_ in t1[:, 1:3] for q in range(a_, b_))
+            assert covered == sorted(part[ss == s_].tolist()) if nch[s_] >= 2 else covered == []
+            if (t1[:, 3] >= 0).any():
+                assert (t1[:, 3] >= 0).all()
+                t2 = r2[r2[:, 0] == s_]
+                assert len(t2) == 1 and list(range(t2[0, 1], t2[0, 2])) == sorted(t1[:, 3].tolist())
