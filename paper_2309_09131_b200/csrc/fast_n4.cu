@@ -1,0 +1,8 @@
+// Fast-path mode-pass instantiations for N = 4 (see fast_kernel.cuh).
+#include "fast_kernel.cuh"
+
+namespace fc {
+int fast_dispatch_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  return dispatch_fast<4>(a, nchunks, st);
+}
+}  // namespace fc

@@ -1,0 +1,95 @@
+// Kernel-side definitions shared by the mode-pass translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace fc {
+
+constexpr int kBlock = 256;
+constexpr int kIPT = 8;
+constexpr int kTile = kBlock * kIPT;  // 2048 elements per tile
+constexpr int64_t kSmemAccBytes = 64 * 1024;
+
+struct ModeArgs {
+  const int4 *src;
+  const float *src_val;
+  int4 *dst;
+  float *dst_val;
+  const float *fac[8];
+  float *out;
+  int nmodes, mode, rank;
+  int64_t out_rows, m;
+  const int64_t *chunk_start;
+  const int32_t *chunk_ss;
+  const int32_t *chunk_part;
+  float *part_ws;
+  const uint32_t *slots;
+  int64_t nnz;
+  int do_remap;
+  int32_t *flags;
+  unsigned long long *counters;
+};
+
+__device__ __forceinline__ int4 ld_stream_v4(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int word_of(const int4 &a, const int4 &b, int w) {
+  switch (w) {
+    case 0: return a.x;
+    case 1: return a.y;
+    case 2: return a.z;
+    case 3: return a.w;
+    case 4: return b.x;
+    case 5: return b.y;
+    case 6: return b.z;
+    default: return b.w;
+  }
+}
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  static __device__ __forceinline__ void load_ro(const float *p, float (&v)[4]) {
+    const float4 f = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+  static __device__ __forceinline__ void load(const float *p, float (&v)[4]) {
+    const float4 f = *reinterpret_cast<const float4 *>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+  static __device__ __forceinline__ void store(float *p, const float (&v)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
+struct VecT<1> {
+  static __device__ __forceinline__ void load_ro(const float *p, float (&v)[1]) { v[0] = __ldg(p); }
+  static __device__ __forceinline__ void load(const float *p, float (&v)[1]) { v[0] = *p; }
+  static __device__ __forceinline__ void store(float *p, const float (&v)[1]) { *p = v[0]; }
+};
+
+constexpr int kMaxBins = 256;
+constexpr int kWarps = kBlock / 32;
+
+// Fast-path launchers, one translation unit per mode count (fast_n*.cu).
+int fast_dispatch_n2(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+int fast_dispatch_n3(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+int fast_dispatch_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+
+}  // namespace fc

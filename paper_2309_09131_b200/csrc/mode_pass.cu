@@ -28,92 +28,13 @@
 // are summed by K2 in chunk order.
 #include <cub/block/block_radix_sort.cuh>
 
-#include "common.cuh"
+#include "mode_args.cuh"
 
 namespace fc {
 namespace {
 
-constexpr int kBlock = 256;
-constexpr int kIPT = 8;
-constexpr int kTile = kBlock * kIPT;  // 2048 elements per tile
 constexpr int kRadixBits = 6;
-constexpr int64_t kSmemAccBytes = 64 * 1024;
-
 using BlockSort = cub::BlockRadixSort<uint32_t, kBlock, kIPT, uint16_t, kRadixBits>;
-
-struct ModeArgs {
-  const int4 *src;
-  const float *src_val;
-  int4 *dst;
-  float *dst_val;
-  const float *fac[8];
-  float *out;
-  int nmodes, mode, rank;
-  int64_t out_rows, m;
-  const int64_t *chunk_start;
-  const int32_t *chunk_ss;
-  const int32_t *chunk_part;
-  float *part_ws;
-  const uint32_t *slots;
-  int64_t nnz;
-  int do_remap;
-  int32_t *flags;
-  unsigned long long *counters;
-};
-
-__device__ __forceinline__ int4 ld_stream_v4(const int4 *p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
-  uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float ld_stream_f32(const float *p) {
-  float r;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ int word_of(const int4 &a, const int4 &b, int w) {
-  switch (w) {
-    case 0: return a.x;
-    case 1: return a.y;
-    case 2: return a.z;
-    case 3: return a.w;
-    case 4: return b.x;
-    case 5: return b.y;
-    case 6: return b.z;
-    default: return b.w;
-  }
-}
-
-template <int VEC>
-struct VecT;
-template <>
-struct VecT<4> {
-  static __device__ __forceinline__ void load_ro(const float *p, float (&v)[4]) {
-    const float4 f = __ldg(reinterpret_cast<const float4 *>(p));
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-  }
-  static __device__ __forceinline__ void load(const float *p, float (&v)[4]) {
-    const float4 f = *reinterpret_cast<const float4 *>(p);
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-  }
-  static __device__ __forceinline__ void store(float *p, const float (&v)[4]) {
-    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-};
-template <>
-struct VecT<1> {
-  static __device__ __forceinline__ void load_ro(const float *p, float (&v)[1]) { v[0] = __ldg(p); }
-  static __device__ __forceinline__ void load(const float *p, float (&v)[1]) { v[0] = *p; }
-  static __device__ __forceinline__ void store(float *p, const float (&v)[1]) { *p = v[0]; }
-};
 
 // Shared-memory plan of one CTA (dynamic smem, carved in this order).
 template <int CW4, bool EMB>
@@ -414,304 +335,6 @@ __global__ void __launch_bounds__(kBlock) mode_pass_kernel(const ModeArgs a) {
 }
 
 
-// ---------------------------------------------------------------------------
-// Fast path (m <= 256 rows per super-shard, N <= 4, R % 4 == 0, R <= 128):
-// stable counting sort of each tile by output row with warp-level match
-// ranking (no block radix sort), records scattered straight into a padded
-// sorted tile, pieces read back conflict-free.  Same phases A-D as above.
-constexpr int kMaxBins = 256;
-constexpr int kWarps = kBlock / 32;
-
-template <int NM, int LPG>
-struct FastPlan {
-  static constexpr int G = kBlock / LPG;
-  static constexpr int P = kTile / G;
-  static constexpr bool EMB = value_embedded(NM);
-  static constexpr size_t sorted_bytes = sizeof(int4) * (kTile + G);
-  static constexpr size_t sval_bytes = EMB ? 0 : sizeof(float) * (kTile + G);
-  static constexpr size_t hist_bytes = sizeof(int) * kWarps * kMaxBins;
-  static constexpr size_t fixed_bytes = sorted_bytes + sval_bytes + hist_bytes + 64;
-  static size_t total(int rank, int64_t m) {
-    return fixed_bytes + (size_t)2 * G * sizeof(int) + (size_t)2 * G * rank * sizeof(float) +
-           (size_t)m * rank * sizeof(float);
-  }
-};
-
-template <int NM, int LPG>
-__global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArgs a) {
-  using FP = FastPlan<NM, LPG>;
-  constexpr int VEC = 4;
-  constexpr int G = FP::G;
-  constexpr int P = FP::P;
-  constexpr bool EMB = FP::EMB;
-  constexpr int U = 4;
-  const int mode = a.mode;
-  const int R = a.rank;
-
-  extern __shared__ __align__(16) unsigned char smem[];
-  int4 *s_sorted = reinterpret_cast<int4 *>(smem);
-  float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
-  int *s_hist = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
-  int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes + FP::hist_bytes);
-  int *s_bnd_row = reinterpret_cast<int *>(smem + FP::fixed_bytes);
-  float *s_bnd = reinterpret_cast<float *>(smem + FP::fixed_bytes + 2 * G * sizeof(int));
-  float *s_acc = reinterpret_cast<float *>(smem + FP::fixed_bytes + 2 * G * sizeof(int) +
-                                           (size_t)2 * G * R * sizeof(float));
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t chunk = blockIdx.x;
-  const int64_t start = a.chunk_start[chunk];
-  const int64_t end = a.chunk_start[chunk + 1];
-  const int64_t ss = a.chunk_ss[chunk];
-  const int part = a.chunk_part[chunk];
-  const int64_t row0 = ss * a.m;
-  const int rows = (int)min64(a.m, a.out_rows - row0);
-
-  for (int i = tid; i < rows * R; i += kBlock) s_acc[i] = 0.f;
-
-  const int gi = tid / LPG;
-  const int lg = tid % LPG;
-  const int col = lg * VEC;
-  const bool col_ok = col < R;
-  auto phys = [](int pos) { return pos + pos / P; };
-  auto row_at = [&](int pos) { return word_of(s_sorted[phys(pos)], s_sorted[phys(pos)], mode) - (int)row0; };
-
-  for (int64_t t0 = start; t0 < end; t0 += kTile) {
-    const int cnt = (int)min64(kTile, end - t0);
-    // ---------------------------------------------------------------- A
-    int4 rec[kIPT];
-    float rv[kIPT];
-    uint32_t slot[kIPT];
-#pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int e = j * kBlock + tid;
-      if (e < cnt) {
-        const int64_t i = t0 + e;
-        rec[j] = ld_stream_v4(a.src + i);
-        if (!EMB) rv[j] = ld_stream_f32(a.src_val + i);
-        if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
-      } else {
-        rec[j] = make_int4(0, 0, 0, 0);
-        rec[j].x = rec[j].y = rec[j].z = rec[j].w = (int)0x80000000;  // never a valid row
-      }
-    }
-    for (int b = lane; b < rows; b += 32) s_hist[warp * kMaxBins + b] = 0;
-    // local row of item j, -1 when padding or outside the super-shard
-    auto key_of = [&](const int4 &r) {
-      const int lr = word_of(r, r, mode) - (int)row0;
-      return (lr >= 0 && lr < rows) ? lr : -1;
-    };
-#pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int e = j * kBlock + tid;
-      if (e < cnt) {
-        if (a.do_remap) {
-          const uint64_t s = slot[j];
-          if (s < (uint64_t)a.nnz) {
-            a.dst[s] = rec[j];
-            if (!EMB) a.dst_val[s] = rv[j];
-          } else {
-            atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
-          }
-        }
-        if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
-      }
-    }
-    __syncwarp();
-    // ---------------------------------------------------------------- B
-    // B1: warp-local stable ranks, order (warp, item j, lane)
-    int lrank[kIPT];
-    int *wh = s_hist + warp * kMaxBins;
-#pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int k = key_of(rec[j]);
-      const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
-      int old = 0;
-      if (k >= 0) old = wh[k];
-      __syncwarp();
-      if (k >= 0 && lane == __ffs(grp) - 1) wh[k] = old + __popc(grp);
-      __syncwarp();
-      lrank[j] = old + __popc(grp & lt_mask);
-    }
-    __syncthreads();
-    // B2: bases[bin][warp] = sum of earlier bins + same bin of earlier warps
-    {
-      int tot = 0;
-      int cw[kWarps];
-      if (tid < rows) {
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          cw[w] = s_hist[w * kMaxBins + tid];
-          tot += cw[w];
-        }
-      }
-      int incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) s_misc[warp] = incl;
-      __syncthreads();
-      int wpre = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
-      if (tid == kBlock - 1) s_misc[kWarps] = wpre + incl;  // nvalid
-      if (tid < rows) {
-        int base = wpre + incl - tot;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          s_hist[w * kMaxBins + tid] = base;
-          base += cw[w];
-        }
-      }
-    }
-    __syncthreads();
-    // B3: scatter records to their sorted (padded) slots
-#pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int k = key_of(rec[j]);
-      if (k >= 0) {
-        const int pos = wh[k] + lrank[j];
-        s_sorted[phys(pos)] = rec[j];
-        if (!EMB) s_sval[phys(pos)] = rv[j];
-      }
-    }
-    __syncthreads();
-    const int nvalid = s_misc[kWarps];
-    // ---------------------------------------------------------------- C
-    if (lg == 0) {
-      s_bnd_row[2 * gi] = -1;
-      s_bnd_row[2 * gi + 1] = -1;
-    }
-    const int pb = gi * P;
-    const int pe = min(pb + P, nvalid);
-    if (pb < nvalid) {
-      int cur = row_at(pb);
-      bool head = pb > 0 && row_at(pb - 1) == cur;
-      float acc[VEC];
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-      auto flush = [&](int row, bool as_head) {
-        if (!col_ok) return;
-        if (as_head) {
-          VecT<VEC>::store(s_bnd + (2 * gi) * R + col, acc);
-        } else {
-          float *p = s_acc + row * R + col;
-          float o[VEC];
-          VecT<VEC>::load(p, o);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) o[v] += acc[v];
-          VecT<VEC>::store(p, o);
-        }
-      };
-      for (int p = pb; p < pe; p += U) {
-        int rowu[U];
-        float vu[U];
-        int cu[U][NM];
-        bool oku[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int pp = p + u;
-          oku[u] = pp < pe;
-          const int ph = phys(oku[u] ? pp : pb);
-          const int4 q = s_sorted[ph];
-#pragma unroll
-          for (int w = 0; w < NM; ++w) cu[u][w] = word_of(q, q, w);
-          rowu[u] = oku[u] ? word_of(q, q, mode) - (int)row0 : -1;
-          vu[u] = EMB ? __int_as_float(q.w) : s_sval[ph];
-        }
-        float pr[U][VEC];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) pr[u][v] = 1.f;
-#pragma unroll
-        for (int w = 0; w < NM; ++w) {
-          if (w == mode) continue;
-          const float *F = a.fac[w];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (oku[u] && col_ok) {
-              float f[VEC];
-              VecT<VEC>::load_ro(F + (int64_t)cu[u][w] * R + col, f);
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) pr[u][v] *= f[v];
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (!oku[u]) break;
-          if (rowu[u] != cur) {
-            flush(cur, head);
-            if (head && lg == 0) s_bnd_row[2 * gi] = cur;
-            head = false;
-            cur = rowu[u];
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-          }
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] += vu[u] * pr[u][v];
-        }
-      }
-      const bool tail = pe < nvalid && row_at(pe) == cur;
-      if (tail && !head) {
-        if (lg == 0) s_bnd_row[2 * gi + 1] = cur;
-        if (col_ok) VecT<VEC>::store(s_bnd + (2 * gi + 1) * R + col, acc);
-      } else {
-        flush(cur, head);
-        if (head && lg == 0) s_bnd_row[2 * gi] = cur;
-      }
-    }
-    __syncthreads();
-    // ---------------------------------------------------------------- D
-    if (warp == 0) {
-      constexpr int RC = (LPG * VEC + 31) / 32;
-      float run[RC];
-#pragma unroll
-      for (int q = 0; q < RC; ++q) run[q] = 0.f;
-      int curr = -1;
-      for (int ent = 0; ent < 2 * G; ++ent) {
-        const int row = s_bnd_row[ent];
-        if (row < 0) continue;
-        if (row != curr) {
-          if (curr >= 0) {
-#pragma unroll
-            for (int q = 0; q < RC; ++q) {
-              const int c = q * 32 + lane;
-              if (c < R) s_acc[curr * R + c] += run[q];
-              run[q] = 0.f;
-            }
-          }
-          curr = row;
-        }
-#pragma unroll
-        for (int q = 0; q < RC; ++q) {
-          const int c = q * 32 + lane;
-          if (c < R) run[q] += s_bnd[ent * R + c];
-        }
-      }
-      if (curr >= 0) {
-#pragma unroll
-        for (int q = 0; q < RC; ++q) {
-          const int c = q * 32 + lane;
-          if (c < R) s_acc[curr * R + c] += run[q];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  float *dstp = part < 0 ? a.out + row0 * R : a.part_ws + (int64_t)part * a.m * R;
-  const int n4 = rows * R / 4;
-  const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
-  float4 *d4 = reinterpret_cast<float4 *>(dstp);
-  for (int i = tid; i < n4; i += kBlock) d4[i] = s4[i];
-  if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
-}
-
 // K2: deterministic two-level reduce of partial tiles.  Level 1: task t
 // sums partials [p0, p1) of super-shard ss (<= kReduceFan of them) in chunk
 // order into out rows (dst < 0) or level-2 slot dst; level 2 sums a
@@ -814,30 +437,6 @@ int launch_mode_pass(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   return FC_OK;
 }
 
-template <int NM, int LPG>
-int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.m);
-  auto kern = mode_pass_fast_kernel<NM, LPG>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  if (nchunks > 0) {
-    kern<<<(unsigned)nchunks, kBlock, smem, st>>>(a);
-    FC_LAUNCH_CHECK();
-  }
-  return FC_OK;
-}
-
-template <int NM>
-int dispatch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const int q = a.rank / 4;
-  if (q <= 4) return launch_fast<NM, 4>(a, nchunks, st);
-  if (q <= 8) return launch_fast<NM, 8>(a, nchunks, st);
-  return launch_fast<NM, 16>(a, nchunks, st);
-}
-
 // Fast path when the accumulator tile is in shared memory, m <= 256,
 // N <= 4 and R % 4 == 0, R <= 64; the general kernel otherwise.
 bool fast_ok(const ModeArgs &a, bool smem_acc) {
@@ -850,9 +449,9 @@ int dispatch(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const int R = a.rank;
   const int N = a.nmodes;
   if (fast_ok(a, SMEM_ACC)) {
-    if (N == 3) return dispatch_fast<3>(a, nchunks, st);
-    if (N == 4) return dispatch_fast<4>(a, nchunks, st);
-    return dispatch_fast<2>(a, nchunks, st);
+    if (N == 3) return fast_dispatch_n3(a, nchunks, st);
+    if (N == 4) return fast_dispatch_n4(a, nchunks, st);
+    return fast_dispatch_n2(a, nchunks, st);
   }
   if (R % 4 == 0 && R <= 32 && N == 3) {
     if (R <= 16) return launch_mode_pass<3, 4, 4, 1, SMEM_ACC>(a, nchunks, st);
