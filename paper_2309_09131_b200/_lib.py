@@ -11,8 +11,11 @@ import ctypes
 import threading
 from pathlib import Path
 
+import os
+
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libflycoo.so"
+# FLYCOO_LIB selects an alternative in-tree build (A/B kernel experiments)
+LIB_PATH = _HERE / os.environ.get("FLYCOO_LIB", "libflycoo.so")
 
 _c = ctypes
 _vp = _c.c_void_p

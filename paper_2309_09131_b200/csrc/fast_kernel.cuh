@@ -13,6 +13,10 @@
 
 #include "mode_args.cuh"
 
+#ifndef FAST_MIN_BLOCKS
+#define FAST_MIN_BLOCKS 3
+#endif
+
 namespace fc {
 
 template <int NM, int LPG>
@@ -22,11 +26,14 @@ struct FastPlan {
   static constexpr bool EMB = value_embedded(NM);
   static constexpr size_t sorted_bytes = sizeof(int4) * (kTile + G);
   static constexpr size_t sval_bytes = EMB ? 0 : sizeof(float) * (kTile + G);
-  static constexpr size_t hist_bytes = sizeof(int) * kWarps * kMaxBins;
-  static constexpr size_t fixed_bytes = sorted_bytes + sval_bytes + hist_bytes + 64;
+  static constexpr size_t misc_bytes = 64;
+  static constexpr size_t fixed_bytes = sorted_bytes + sval_bytes + misc_bytes;
+  // dynamic tail: per-warp row histograms (m ints each), boundary entries,
+  // the m x R accumulator tile
+  __host__ __device__ static size_t hist_bytes(int64_t m) { return sizeof(int) * kWarps * ((m + 3) / 4 * 4); }
   static size_t total(int rank, int64_t m) {
-    return fixed_bytes + (size_t)2 * G * sizeof(int) + (size_t)2 * G * rank * sizeof(float) +
-           (size_t)m * rank * sizeof(float);
+    return fixed_bytes + hist_bytes(m) + (size_t)2 * G * sizeof(int) +
+           (size_t)2 * G * rank * sizeof(float) + (size_t)m * rank * sizeof(float);
   }
 };
 
@@ -68,7 +75,7 @@ __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, 
 }
 
 template <int NM, int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArgs a) {
+__global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const ModeArgs a) {
   using FP = FastPlan<NM, LPG>;
   constexpr int G = FP::G;
   constexpr int P = FP::P;
@@ -77,14 +84,18 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
+  const int hstride = (int)((a.m + 3) / 4 * 4);
   int4 *s_sorted = reinterpret_cast<int4 *>(smem);
   float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
-  int *s_hist = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
-  int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes + FP::hist_bytes);
-  int *s_bnd_row = reinterpret_cast<int *>(smem + FP::fixed_bytes);
-  float *s_bnd = reinterpret_cast<float *>(smem + FP::fixed_bytes + 2 * G * sizeof(int));
-  float *s_acc = reinterpret_cast<float *>(smem + FP::fixed_bytes + 2 * G * sizeof(int) +
-                                           (size_t)2 * G * R * sizeof(float));
+  int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
+  unsigned char *tail = smem + FP::fixed_bytes;
+  int *s_hist = reinterpret_cast<int *>(tail);
+  tail += FP::hist_bytes(a.m);
+  int *s_bnd_row = reinterpret_cast<int *>(tail);
+  tail += 2 * G * sizeof(int);
+  float *s_bnd = reinterpret_cast<float *>(tail);
+  tail += (size_t)2 * G * R * sizeof(float);
+  float *s_acc = reinterpret_cast<float *>(tail);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
         rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
       }
     }
-    for (int b = lane; b < rows; b += 32) s_hist[warp * kMaxBins + b] = 0;
+    for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
 #pragma unroll
     for (int j = 0; j < kIPT; ++j) {
       const int e = j * kBlock + tid;
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
     // B1: warp-local ranks.  The rank is parked in the record's mode word
     // as (rank << 8 | local row) until B3 restores the coordinate -- keeps
     // the 8 ranks out of registers.
-    int *wh = s_hist + warp * kMaxBins;
+    int *wh = s_hist + warp * hstride;
 #pragma unroll
     for (int j = 0; j < kIPT; ++j) {
       const int k = key_of(rec[j]);
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
       if (tid < rows) {
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-          cw[w] = s_hist[w * kMaxBins + tid];
+          cw[w] = s_hist[w * hstride + tid];
           tot += cw[w];
         }
       }
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
         int base = wpre + incl - tot;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-          s_hist[w * kMaxBins + tid] = base;
+          s_hist[w * hstride + tid] = base;
           base += cw[w];
         }
       }
@@ -277,38 +288,51 @@ __global__ void __launch_bounds__(kBlock, 3) mode_pass_fast_kernel(const ModeArg
     }
     __syncthreads();
     // ---------------------------------------------------------------- D
-    if (warp == 0) {
+    // Boundary entries are in sorted-row order (H0 T0 H1 T1 ...).  Warp w
+    // folds every run of equal rows that *starts* in entries
+    // [w * E, (w + 1) * E), in entry order -- same sums as one warp walking
+    // all entries, spread over the CTA.
+    {
+      constexpr int E = (2 * G + kWarps - 1) / kWarps;
       constexpr int RC = (LPG * 4 + 31) / 32;
-      float run[RC];
-#pragma unroll
-      for (int q = 0; q < RC; ++q) run[q] = 0.f;
-      int curr = -1;
-      for (int ent = 0; ent < 2 * G; ++ent) {
-        const int row = s_bnd_row[ent];
-        if (row < 0) continue;
-        if (row != curr) {
-          if (curr >= 0) {
-#pragma unroll
-            for (int q = 0; q < RC; ++q) {
-              const int c = q * 32 + lane;
-              if (c < R) s_acc[curr * R + c] += run[q];
-              run[q] = 0.f;
-            }
-          }
-          curr = row;
-        }
-#pragma unroll
-        for (int q = 0; q < RC; ++q) {
-          const int c = q * 32 + lane;
-          if (c < R) run[q] += s_bnd[ent * R + c];
+      int ent = warp * E;
+      const int ent_end = min(2 * G, ent + E);
+      int prev = -1;
+      for (int e2 = ent - 1; e2 >= 0; --e2) {  // row of the last valid entry before my range
+        const int r2 = s_bnd_row[e2];
+        if (r2 >= 0) {
+          prev = r2;
+          break;
         }
       }
-      if (curr >= 0) {
+      while (ent < ent_end) {
+        const int row = s_bnd_row[ent];
+        if (row < 0 || row == prev) {  // invalid, or continues a run started earlier
+          if (row >= 0) prev = row;
+          ++ent;
+          continue;
+        }
+        float run[RC];
+#pragma unroll
+        for (int q = 0; q < RC; ++q) run[q] = 0.f;
+        int e3 = ent;
+        for (; e3 < 2 * G; ++e3) {
+          const int r3 = s_bnd_row[e3];
+          if (r3 < 0) continue;
+          if (r3 != row) break;
+#pragma unroll
+          for (int q = 0; q < RC; ++q) {
+            const int c = q * 32 + lane;
+            if (c < R) run[q] += s_bnd[e3 * R + c];
+          }
+        }
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
           const int c = q * 32 + lane;
-          if (c < R) s_acc[curr * R + c] += run[q];
+          if (c < R) s_acc[row * R + c] += run[q];
         }
+        prev = row;
+        ent = e3;
       }
     }
   }
