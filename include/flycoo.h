@@ -78,6 +78,8 @@ int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
  *   acc_in_smem must be 1 iff m_mode <= fc_smem_acc_rows_max(rank); with
  *   acc_in_smem == 0 every chunk must own its super-shard and `out` must be
  *   zero on entry.
+ * Slots must be < nnz, the destination capacity (on one GPU the buffer
+ * size; multi-GPU: local part + send region, see dist.py).
  * counters[0] += elements processed (the engine.py:335-338 check).        */
 int fc_mode_worker(const void *src_crd, const float *src_val,
                    void *dst_crd, float *dst_val,
@@ -100,6 +102,13 @@ int fc_remap_cursor(const void *src_crd, const float *src_val, void *dst_crd,
                     float *dst_val, const uint32_t *src_sid, uint32_t *dst_sid,
                     int nmodes, int next_mode, int64_t nnz, const int64_t *dest_base,
                     unsigned long long *cursors, int32_t *flags, void *stream);
+
+/* Receiver-side unpack of the multi-GPU remap: dst[slots[k]] = src[k] for
+ * k < n, slots < dst_capacity; counters[0] += n. */
+int fc_scatter_records(const void *src_crd, const float *src_val, int64_t n,
+                       void *dst_crd, float *dst_val, int64_t dst_capacity,
+                       const uint32_t *slots, int nmodes, int32_t *flags,
+                       unsigned long long *counters, void *stream);
 
 /* ---------------------------------------------------------------- K5 build
  * Layout build (layout.py:462-531) in device passes; the host shim

@@ -42,6 +42,7 @@ _SIGS = {
         _int, _int, _int,              # do_compute, do_remap, acc_in_smem
         _vp, _vp, _vp]),               # flags, counters, stream
     "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),
+    "fc_scatter_records": (_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _int, _vp, _vp, _vp]),
     "fc_build_morton": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fc_build_sort_temp_bytes": (_i64, [_i64]),
     "fc_build_sort_pairs": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp]),

@@ -371,14 +371,14 @@ __global__ void __launch_bounds__(256) reduce_level_kernel(const int64_t *tasks,
 template <int CW4, bool EMB>
 __global__ void __launch_bounds__(256) remap_only_kernel(const int4 *src, const float *src_val,
                                                          int4 *dst, float *dst_val,
-                                                         const uint32_t *slots, int64_t nnz,
-                                                         int32_t *flags,
+                                                         const uint32_t *slots, int64_t n,
+                                                         int64_t dst_cap, int32_t *flags,
                                                          unsigned long long *counters) {
   unsigned done = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t s = ld_stream_u32(slots + i);
-    if (s >= (uint64_t)nnz) {
+    if (s >= (uint64_t)dst_cap) {
       atomicOr(flags, FC_FLAG_SLOT_RANGE);
       ++done;
       continue;
@@ -500,13 +500,13 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
     auto src4 = static_cast<const int4 *>(src_crd);
     auto dst4 = static_cast<int4 *>(dst_crd);
     if (cw4 == 1 && emb)
-      remap_only_kernel<1, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, flags, counters);
+      remap_only_kernel<1, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
     else if (cw4 == 1)
-      remap_only_kernel<1, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, flags, counters);
+      remap_only_kernel<1, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
     else if (emb)
-      remap_only_kernel<2, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, flags, counters);
+      remap_only_kernel<2, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
     else
-      remap_only_kernel<2, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, flags, counters);
+      remap_only_kernel<2, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
     FC_LAUNCH_CHECK();
     return FC_OK;
   }
@@ -585,6 +585,31 @@ int fc_remap_cursor(const void *src_crd, const float *src_val, void *dst_crd, fl
   else if (emb) FC_CURSOR(2, true);
   else FC_CURSOR(2, false);
 #undef FC_CURSOR
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_scatter_records(const void *src_crd, const float *src_val, int64_t n, void *dst_crd,
+                       float *dst_val, int64_t dst_capacity, const uint32_t *slots, int nmodes,
+                       int32_t *flags, unsigned long long *counters, void *stream) {
+  FC_CHECK_ARG(nmodes >= 2 && nmodes <= 8, "nmodes %d outside [2, 8]", nmodes);
+  FC_CHECK_ARG(n == 0 || (src_crd && dst_crd && slots && flags && counters), "null buffer");
+  const int cw4 = crd_words(nmodes) / 4;
+  const bool emb = value_embedded(nmodes);
+  FC_CHECK_ARG(emb || n == 0 || (src_val && dst_val), "N=%d needs value arrays", nmodes);
+  if (n == 0) return FC_OK;
+  cudaStream_t st = as_stream(stream);
+  const int grid = (int)min64((n + 255) / 256, 148 * 16);
+  auto s4 = static_cast<const int4 *>(src_crd);
+  auto d4 = static_cast<int4 *>(dst_crd);
+  if (cw4 == 1 && emb)
+    remap_only_kernel<1, true><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
+  else if (cw4 == 1)
+    remap_only_kernel<1, false><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
+  else if (emb)
+    remap_only_kernel<2, true><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
+  else
+    remap_only_kernel<2, false><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
   FC_LAUNCH_CHECK();
   return FC_OK;
 }

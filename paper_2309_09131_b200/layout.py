@@ -148,6 +148,13 @@ def reduce_plan(nch: np.ndarray, part_base: np.ndarray, fan: int = REDUCE_FAN):
     return r1, r2, slot
 
 
+def default_chunk_elems(nnz: int, tile: int = 2048) -> int:
+    """Chunk size: 8192 elements, smaller for small tensors so that every
+    SM gets work (multiples of the 2048-element tile)."""
+    want = _cdiv(max(int(nnz), 1), 148 * 4)
+    return int(min(8192, max(tile, _cdiv(want, tile) * tile)))
+
+
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None) -> ModeWork:
     """Split every super-shard of `mode` into CTA chunks.  Shared-memory
     accumulation (m rows fit): chunks of `chunk_elems`, super-shards with
@@ -164,8 +171,7 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
     smem = m <= int(L.fc_smem_acc_rows_max(int(rank)))
     if smem:
         if chunk_elems is None:
-            want = _cdiv(max(nnz, 1), 148 * 4)
-            chunk_elems = int(min(8192, max(tile, _cdiv(want, tile) * tile)))
+            chunk_elems = default_chunk_elems(nnz, tile)
         C = int(chunk_elems)
         nch = -(-counts // C)
     else:
