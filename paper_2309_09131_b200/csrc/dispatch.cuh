@@ -1,0 +1,51 @@
+// Fast-path dispatch: (N, mode, R) -> kernel instance.  The one-CTA-per-chunk
+// tile kernel (fast_kernel.cuh) is the default; FLYCOO_KERNEL=pipe selects the
+// persistent warp-specialised pipeline (pipe_kernel.cuh) for A/B runs
+// (round 1: 5.50 vs 5.18 ms per c2 sweep, the tile kernel wins).
+#pragma once
+
+#include <stdlib.h>
+#include <string.h>
+
+#include "pipe_kernel.cuh"
+
+namespace fc {
+
+inline bool use_tile_kernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("FLYCOO_KERNEL");
+    v = (e && strcmp(e, "pipe") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int NM, int MODE, int LPG, int RT>
+int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  if (use_tile_kernel()) return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
+  return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);
+}
+
+template <int NM, int MODE>
+int dispatch_fast_mode(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  if (a.rank == 32) return launch_choice<NM, MODE, 8, 32>(a, nchunks, st);
+  if (a.rank == 16) return launch_choice<NM, MODE, 4, 16>(a, nchunks, st);
+  return launch_choice<NM, MODE, 16, 0>(a, nchunks, st);  // any R % 4 == 0 up to 64
+}
+
+template <int NM>
+int dispatch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  switch (a.mode) {
+    case 0: return dispatch_fast_mode<NM, 0>(a, nchunks, st);
+    case 1: return dispatch_fast_mode<NM, 1>(a, nchunks, st);
+    case 2: if constexpr (NM > 2) return dispatch_fast_mode<NM, (NM > 2 ? 2 : 0)>(a, nchunks, st);
+            break;
+    case 3: if constexpr (NM > 3) return dispatch_fast_mode<NM, (NM > 3 ? 3 : 0)>(a, nchunks, st);
+            break;
+    default: break;
+  }
+  set_error("fast path: mode %d out of range for N=%d", a.mode, NM);
+  return FC_ERR_ARG;
+}
+
+}  // namespace fc

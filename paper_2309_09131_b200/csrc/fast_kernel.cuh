@@ -51,11 +51,10 @@ __device__ __forceinline__ void set_comp(int4 &q, int v) {
   else q.w = v;
 }
 
-// Gather the N-1 factor row slices of one element and return v * prod.
+// Gather the N-1 factor row slices of one element: pr = prod_{w != mode} F_w[c_w, col:col+4].
 template <int NM, int MODE, int RT>
-__device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, const int4 &q,
-                                             float v, float (&t)[4]) {
-  float pr[4];
+__device__ __forceinline__ void element_prod(const ModeArgs &a, int R, int col, const int4 &q,
+                                             float (&pr)[4]) {
   bool first = true;
 #pragma unroll
   for (int w = 0; w < NM; ++w) {
@@ -70,6 +69,14 @@ __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, 
       pr[0] *= f.x; pr[1] *= f.y; pr[2] *= f.z; pr[3] *= f.w;
     }
   }
+}
+
+// Reference-compatible name used by the pipeline kernel: t = v * prod.
+template <int NM, int MODE, int RT>
+__device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, const int4 &q,
+                                             float v, float (&t)[4]) {
+  float pr[4];
+  element_prod<NM, MODE, RT>(a, R, col, q, pr);
 #pragma unroll
   for (int k = 0; k < 4; ++k) t[k] = v * pr[k];
 }
@@ -243,40 +250,43 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
           VecT<4>::store(p, o);
         }
       };
-      auto consume = [&](int row, const float (&t)[4]) {
+      auto consume = [&](int row, float v, const float (&pr)[4]) {
         if (row != cur) {
           flush();
           head = false;
           cur = row;
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[v] = 0.f;
+          for (int k = 0; k < 4; ++k) acc[k] = 0.f;
         }
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[v] += t[v];
+        for (int k = 0; k < 4; ++k) acc[k] = fmaf(v, pr[k], acc[k]);
       };
+      // positions of one piece share the pad: phys(p) = p + gi for p in [pb, pb + P)
+      const int4 *sp = s_sorted + gi;
+      const float *svp = s_sval + gi;
       int p = pb;
       for (; p + U <= pe; p += U) {
         int4 q[U];
         float vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          q[u] = s_sorted[phys(p + u)];
-          vv[u] = EMB ? __int_as_float(q[u].w) : s_sval[phys(p + u)];
+          q[u] = sp[p + u];
+          vv[u] = EMB ? __int_as_float(q[u].w) : svp[p + u];
         }
-        float t[U][4];
+        float pr[U][4];
         if (col_ok) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) element_term<NM, MODE, RT>(a, R, col, q[u], vv[u], t[u]);
+          for (int u = 0; u < U; ++u) element_prod<NM, MODE, RT>(a, R, col, q[u], pr[u]);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), t[u]);
+        for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
       }
       for (; p < pe; ++p) {
-        const int4 q = s_sorted[phys(p)];
-        const float vv = EMB ? __int_as_float(q.w) : s_sval[phys(p)];
-        float t[4];
-        if (col_ok) element_term<NM, MODE, RT>(a, R, col, q, vv, t);
-        consume(comp<MODE>(q), t);
+        const int4 q = sp[p];
+        const float vv = EMB ? __int_as_float(q.w) : svp[p];
+        float pr[4];
+        if (col_ok) element_prod<NM, MODE, RT>(a, R, col, q, pr);
+        consume(comp<MODE>(q), vv, pr);
       }
       const bool tail = pe < nvalid && comp<MODE>(s_sorted[phys(pe)]) == cur;
       if (tail && !head) {
@@ -359,28 +369,6 @@ int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     FC_LAUNCH_CHECK();
   }
   return FC_OK;
-}
-
-template <int NM, int MODE>
-int dispatch_fast_mode(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  if (a.rank == 32) return launch_fast<NM, MODE, 8, 32>(a, nchunks, st);
-  if (a.rank == 16) return launch_fast<NM, MODE, 4, 16>(a, nchunks, st);
-  return launch_fast<NM, MODE, 16, 0>(a, nchunks, st);  // any R % 4 == 0 up to 64
-}
-
-template <int NM>
-int dispatch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  switch (a.mode) {
-    case 0: return dispatch_fast_mode<NM, 0>(a, nchunks, st);
-    case 1: return dispatch_fast_mode<NM, 1>(a, nchunks, st);
-    case 2: if constexpr (NM > 2) return dispatch_fast_mode<NM, (NM > 2 ? 2 : 0)>(a, nchunks, st);
-            break;
-    case 3: if constexpr (NM > 3) return dispatch_fast_mode<NM, (NM > 3 ? 3 : 0)>(a, nchunks, st);
-            break;
-    default: break;
-  }
-  set_error("fast path: mode %d out of range for N=%d", a.mode, NM);
-  return FC_ERR_ARG;
 }
 
 }  // namespace fc

@@ -1,5 +1,5 @@
 // Fast-path mode-pass instantiations for N = 2 (see fast_kernel.cuh).
-#include "fast_kernel.cuh"
+#include "dispatch.cuh"
 
 namespace fc {
 int fast_dispatch_n2(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {

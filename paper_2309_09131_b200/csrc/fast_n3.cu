@@ -1,5 +1,5 @@
 // Fast-path mode-pass instantiations for N = 3 (see fast_kernel.cuh).
-#include "fast_kernel.cuh"
+#include "dispatch.cuh"
 
 namespace fc {
 int fast_dispatch_n3(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
