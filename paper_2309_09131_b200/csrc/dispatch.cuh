@@ -8,22 +8,29 @@
 #include <string.h>
 
 #include "pipe_kernel.cuh"
+#include "warp_kernel.cuh"
 
 namespace fc {
 
-inline bool use_tile_kernel() {
+// 0 = warp-independent (default), 1 = tile, 2 = pipeline
+inline int kernel_kind() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("FLYCOO_KERNEL");
-    v = (e && strcmp(e, "pipe") == 0) ? 0 : 1;
+    v = 0;
+    if (e && strcmp(e, "tile") == 0) v = 1;
+    if (e && strcmp(e, "pipe") == 0) v = 2;
   }
-  return v == 1;
+  return v;
 }
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  if (use_tile_kernel()) return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
-  return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);
+  switch (kernel_kind()) {
+    case 1: return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
+    case 2: return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);
+    default: return launch_warp<NM, MODE, LPG, RT>(a, nchunks, st);
+  }
 }
 
 template <int NM, int MODE>

@@ -16,21 +16,40 @@
 #ifndef FAST_MIN_BLOCKS
 #define FAST_MIN_BLOCKS 3
 #endif
+#ifndef FAST_U
+#define FAST_U 4
+#endif
+#ifndef FAST_IPT
+#define FAST_IPT 8
+#endif
 
 namespace fc {
 
+#ifndef FAST_BLOCK
+#define FAST_BLOCK 256
+#endif
+// fast-path tile: kFBlock threads x kFIPT records
+constexpr int kFBlock = FAST_BLOCK;
+constexpr int kFWarps = kFBlock / 32;
+constexpr int kFIPT = FAST_IPT;
+constexpr int kFTile = kFBlock * kFIPT;
+
+#ifdef FAST_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[5];
+#endif
+
 template <int NM, int LPG>
 struct FastPlan {
-  static constexpr int G = kBlock / LPG;
-  static constexpr int P = kTile / G;
+  static constexpr int G = kFBlock / LPG;
+  static constexpr int P = kFTile / G;
   static constexpr bool EMB = value_embedded(NM);
-  static constexpr size_t sorted_bytes = sizeof(int4) * (kTile + G);
-  static constexpr size_t sval_bytes = EMB ? 0 : sizeof(float) * (kTile + G);
-  static constexpr size_t misc_bytes = 64;
+  static constexpr size_t sorted_bytes = sizeof(int4) * (kFTile + G);
+  static constexpr size_t sval_bytes = EMB ? 0 : sizeof(float) * (kFTile + G);
+  static constexpr size_t misc_bytes = 4 * (kFWarps + 4);
   static constexpr size_t fixed_bytes = sorted_bytes + sval_bytes + misc_bytes;
   // dynamic tail: per-warp row histograms (m ints each), boundary entries,
   // the m x R accumulator tile
-  __host__ __device__ static size_t hist_bytes(int64_t m) { return sizeof(int) * kWarps * ((m + 3) / 4 * 4); }
+  __host__ __device__ static size_t hist_bytes(int64_t m) { return sizeof(int) * kFWarps * ((m + 3) / 4 * 4); }
   static size_t total(int rank, int64_t m) {
     return fixed_bytes + hist_bytes(m) + (size_t)2 * G * sizeof(int) +
            (size_t)2 * G * rank * sizeof(float) + (size_t)m * rank * sizeof(float);
@@ -60,8 +79,12 @@ __device__ __forceinline__ void element_prod(const ModeArgs &a, int R, int col, 
   for (int w = 0; w < NM; ++w) {
     if (w == MODE) continue;
     const int c = w == 0 ? q.x : w == 1 ? q.y : w == 2 ? q.z : q.w;
+#ifdef FAST_NO_GATHER  // experiment only: no factor loads
+    const float4 f = make_float4(__int_as_float(c), 1.f, 1.f, 1.f);
+#else
     const float *F = a.fac[w] + (uint64_t)(uint32_t)c * (uint32_t)(RT > 0 ? RT : R) + col;
     const float4 f = __ldg(reinterpret_cast<const float4 *>(F));
+#endif
     if (first) {
       pr[0] = f.x; pr[1] = f.y; pr[2] = f.z; pr[3] = f.w;
       first = false;
@@ -82,12 +105,12 @@ __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, 
 }
 
 template <int NM, int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const ModeArgs a) {
+__global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const ModeArgs a) {
   using FP = FastPlan<NM, LPG>;
   constexpr int G = FP::G;
   constexpr int P = FP::P;
   constexpr bool EMB = FP::EMB;
-  constexpr int U = 4;
+  constexpr int U = FAST_U;
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -116,7 +139,7 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
   const int rows = (int)min64(a.m, a.out_rows - row0);
   const int irow0 = (int)row0;
 
-  for (int i = tid; i < rows * R; i += kBlock) s_acc[i] = 0.f;
+  for (int i = tid; i < rows * R; i += kFBlock) s_acc[i] = 0.f;
 
   const int gi = tid / LPG;
   const int lg = tid % LPG;
@@ -128,15 +151,22 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
     return (lr >= 0 && lr < rows) ? lr : -1;
   };
 
-  for (int64_t t0 = start; t0 < end; t0 += kTile) {
-    const int cnt = (int)min64(kTile, end - t0);
+#ifdef FAST_PHASE_TIMING
+  unsigned long long ph_acc[5] = {0, 0, 0, 0, 0};
+  long long ph_t = clock64();
+#define FAST_PROBE(k) do { if (tid == 0) { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } } while (0)
+#else
+#define FAST_PROBE(k) do { } while (0)
+#endif
+  for (int64_t t0 = start; t0 < end; t0 += kFTile) {
+    const int cnt = (int)min64(kFTile, end - t0);
     // ---------------------------------------------------------------- A
-    int4 rec[kIPT];
-    float rv[kIPT];
-    uint32_t slot[kIPT];
+    int4 rec[kFIPT];
+    float rv[kFIPT];
+    uint32_t slot[kFIPT];
 #pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int e = j * kBlock + tid;
+    for (int j = 0; j < kFIPT; ++j) {
+      const int e = j * kFBlock + tid;
       if (e < cnt) {
         const int64_t i = t0 + e;
         rec[j] = ld_stream_v4(a.src + i);
@@ -148,8 +178,8 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
     }
     for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
 #pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
-      const int e = j * kBlock + tid;
+    for (int j = 0; j < kFIPT; ++j) {
+      const int e = j * kFBlock + tid;
       if (e < cnt) {
         if (a.do_remap) {
           const uint64_t s = slot[j];
@@ -165,12 +195,25 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
     }
     __syncwarp();
     // ---------------------------------------------------------------- B
+#ifdef FAST_NO_SORT  // experiment only: records stay in tile order
+    {
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        const int e = j * kFBlock + tid;
+        if (e < cnt) s_sorted[e + e / P] = rec[j];
+      }
+      if (tid == 0) s_misc[kFWarps] = cnt;
+      __syncthreads();
+    }
+    if (false)
+#endif
+    {
     // B1: warp-local ranks.  The rank is parked in the record's mode word
     // as (rank << 8 | local row) until B3 restores the coordinate -- keeps
     // the 8 ranks out of registers.
     int *wh = s_hist + warp * hstride;
 #pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
+    for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
       int old = 0;
@@ -181,15 +224,12 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
+    FAST_PROBE(0);
     {
       int tot = 0;
-      int cw[kWarps];
       if (tid < rows) {
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-          cw[w] = s_hist[w * hstride + tid];
-          tot += cw[w];
-        }
+#pragma unroll 4
+        for (int w = 0; w < kFWarps; ++w) tot += s_hist[w * hstride + tid];
       }
       int incl = tot;
 #pragma unroll
@@ -200,21 +240,23 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
       if (lane == 31) s_misc[warp] = incl;
       __syncthreads();
       int wpre = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
-      if (tid == kBlock - 1) s_misc[kWarps] = wpre + incl;
+#pragma unroll 4
+      for (int w = 0; w < kFWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
+      if (tid == kFBlock - 1) s_misc[kFWarps] = wpre + incl;
       if (tid < rows) {
         int base = wpre + incl - tot;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
+#pragma unroll 4
+        for (int w = 0; w < kFWarps; ++w) {
+          const int c = s_hist[w * hstride + tid];
           s_hist[w * hstride + tid] = base;
-          base += cw[w];
+          base += c;
         }
       }
     }
     __syncthreads();
+    FAST_PROBE(1);
 #pragma unroll
-    for (int j = 0; j < kIPT; ++j) {
+    for (int j = 0; j < kFIPT; ++j) {
       const int x = comp<MODE>(rec[j]);
       if (x >= 0) {
         const int k = x & 255;
@@ -225,15 +267,34 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
       }
     }
     __syncthreads();
-    const int nvalid = s_misc[kWarps];
+    FAST_PROBE(2);
+    }
+    const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
+    if (tid == 0 && t0 + kFTile < end) {  // next tile's records + slots -> L2
+      const int64_t n1 = min64(kFTile, end - (t0 + kFTile));
+      prefetch_l2(a.src + (t0 + kFTile), n1 * sizeof(int4));
+      if (a.do_remap) prefetch_l2(a.slots + (t0 + kFTile), n1 * sizeof(uint32_t));
+      if (!EMB) prefetch_l2(a.src_val + (t0 + kFTile), n1 * sizeof(float));
+    }
+    // both boundary entries of every group are (re)written this tile: rows
+    // -1 and zero vectors unless a segment lands there
     if (lg == 0) {
       s_bnd_row[2 * gi] = -1;
       s_bnd_row[2 * gi + 1] = -1;
     }
+    if (col_ok) {
+      const float z[4] = {0.f, 0.f, 0.f, 0.f};
+      VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
+      VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
+    }
     const int pb = gi * P;
+#ifdef FAST_NO_C  // experiment only
+    const int pe = pb;
+#else
     const int pe = min(pb + P, nvalid);
-    if (pb < nvalid) {
+#endif
+    if (pb < pe) {
       int cur = comp<MODE>(s_sorted[phys(pb)]);
       bool head = pb > 0 && comp<MODE>(s_sorted[phys(pb - 1)]) == cur;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -265,6 +326,43 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
       const int4 *sp = s_sorted + gi;
       const float *svp = s_sval + gi;
       int p = pb;
+#ifdef FAST_SWP
+      // software pipeline (distance 1): block b+1's record loads and gathers
+      // are issued before block b is consumed
+      if (p + U <= pe) {
+        int4 qa[U], qb[U];
+        float va[U], vb[U];
+        float pa[U][4], pb_[U][4];
+        auto fetch = [&](int at, int4 (&q)[U], float (&vv)[U], float (&pr)[U][4]) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            q[u] = sp[at + u];
+            vv[u] = EMB ? __int_as_float(q[u].w) : svp[at + u];
+          }
+          if (col_ok) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) element_prod<NM, MODE, RT>(a, R, col, q[u], pr[u]);
+          }
+        };
+        fetch(p, qa, va, pa);
+        p += U;
+        while (true) {
+          const bool more = p + U <= pe;
+          if (more) fetch(p, qb, vb, pb_);
+#pragma unroll
+          for (int u = 0; u < U; ++u) consume(comp<MODE>(qa[u]), va[u], pa[u]);
+          if (!more) break;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            qa[u] = qb[u];
+            va[u] = vb[u];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) pa[u][k] = pb_[u][k];
+          }
+          p += U;
+        }
+      }
+#else
       for (; p + U <= pe; p += U) {
         int4 q[U];
         float vv[U];
@@ -281,6 +379,7 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
       }
+#endif
       for (; p < pe; ++p) {
         const int4 q = sp[p];
         const float vv = EMB ? __int_as_float(q.w) : svp[p];
@@ -297,62 +396,71 @@ __global__ void __launch_bounds__(kBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel
       }
     }
     __syncthreads();
+    FAST_PROBE(3);
     // ---------------------------------------------------------------- D
-    // Boundary entries are in sorted-row order (H0 T0 H1 T1 ...).  Warp w
-    // folds every run of equal rows that *starts* in entries
-    // [w * E, (w + 1) * E), in entry order -- same sums as one warp walking
-    // all entries, spread over the CTA.
+    // Boundary entries are in sorted-row order (H0 T0 H1 T1 ...), unused ones
+    // hold zeros.  Warp w folds every run of equal rows that *starts* in
+    // entries [w * E, (w + 1) * E): find the run's end from the row array,
+    // then sum its entries in entry order with independent loads.
     {
-      constexpr int E = (2 * G + kWarps - 1) / kWarps;
+      constexpr int E = (2 * G + kFWarps - 1) / kFWarps;
       constexpr int RC = (LPG * 4 + 31) / 32;
-      int ent = warp * E;
-      const int ent_end = min(2 * G, ent + E);
+      const int ent0 = warp * E;
+      const int ent_end = min(2 * G, ent0 + E);
       int prev = -1;
-      for (int e2 = ent - 1; e2 >= 0; --e2) {  // row of the last valid entry before my range
+      for (int e2 = ent0 - 1; e2 >= 0; --e2) {
         const int r2 = s_bnd_row[e2];
         if (r2 >= 0) {
           prev = r2;
           break;
         }
       }
-      while (ent < ent_end) {
+      for (int ent = ent0; ent < ent_end; ++ent) {
         const int row = s_bnd_row[ent];
-        if (row < 0 || row == prev) {  // invalid, or continues a run started earlier
+        if (row < 0 || row == prev) {
           if (row >= 0) prev = row;
-          ++ent;
           continue;
         }
-        float run[RC];
-#pragma unroll
-        for (int q = 0; q < RC; ++q) run[q] = 0.f;
-        int e3 = ent;
-        for (; e3 < 2 * G; ++e3) {
+        prev = row;
+        int e3 = ent + 1;
+        while (e3 < 2 * G) {
           const int r3 = s_bnd_row[e3];
-          if (r3 < 0) continue;
-          if (r3 != row) break;
-#pragma unroll
-          for (int q = 0; q < RC; ++q) {
-            const int c = q * 32 + lane;
-            if (c < R) run[q] += s_bnd[e3 * R + c];
-          }
+          if (r3 >= 0 && r3 != row) break;
+          ++e3;
         }
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
           const int c = q * 32 + lane;
-          if (c < R) s_acc[row * R + c] += run[q];
+          if (c < R) {
+            float run = 0.f;
+            int e = ent;
+            for (; e + 4 <= e3; e += 4) {
+              const float x0 = s_bnd[e * R + c], x1 = s_bnd[(e + 1) * R + c];
+              const float x2 = s_bnd[(e + 2) * R + c], x3 = s_bnd[(e + 3) * R + c];
+              run += x0;
+              run += x1;
+              run += x2;
+              run += x3;
+            }
+            for (; e < e3; ++e) run += s_bnd[e * R + c];
+            s_acc[row * R + c] += run;
+          }
         }
-        prev = row;
-        ent = e3;
       }
     }
+    FAST_PROBE(4);
   }
   __syncthreads();
   float *dstp = part < 0 ? a.out + row0 * R : a.part_ws + (int64_t)part * a.m * R;
   const int n4 = rows * R / 4;
   const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
   float4 *d4 = reinterpret_cast<float4 *>(dstp);
-  for (int i = tid; i < n4; i += kBlock) d4[i] = s4[i];
+  for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
+#ifdef FAST_PHASE_TIMING
+  if (tid == 0)
+    for (int k = 0; k < 5; ++k) atomicAdd(&g_phase_cycles[k], ph_acc[k]);
+#endif
 }
 
 template <int NM, int MODE, int LPG, int RT>
@@ -365,7 +473,7 @@ int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     configured = smem;
   }
   if (nchunks > 0) {
-    kern<<<(unsigned)nchunks, kBlock, smem, st>>>(a);
+    kern<<<(unsigned)nchunks, kFBlock, smem, st>>>(a);
     FC_LAUNCH_CHECK();
   }
   return FC_OK;

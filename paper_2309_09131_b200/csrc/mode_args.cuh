@@ -48,6 +48,15 @@ __device__ __forceinline__ float ld_stream_f32(const float *p) {
   return r;
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (TMA unit).  The instruction
+// needs a 16-B aligned address and a multiple of 16 bytes: widen the range.
+__device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes) {
+  const uint64_t a0 = reinterpret_cast<uint64_t>(p) & ~uint64_t(15);
+  const uint64_t a1 = (reinterpret_cast<uint64_t>(p) + (uint64_t)bytes + 15) & ~uint64_t(15);
+  const uint32_t n = (uint32_t)(a1 - a0);
+  if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ int word_of(const int4 &a, const int4 &b, int w) {
   switch (w) {
     case 0: return a.x;

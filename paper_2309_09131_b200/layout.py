@@ -26,6 +26,7 @@ entry points of libflycoo (radix sorts, histograms, scatters).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -151,8 +152,9 @@ def reduce_plan(nch: np.ndarray, part_base: np.ndarray, fan: int = REDUCE_FAN):
 def default_chunk_elems(nnz: int, tile: int = 2048) -> int:
     """Chunk size: 8192 elements, smaller for small tensors so that every
     SM gets work (multiples of the 2048-element tile)."""
+    cap = int(os.environ.get("FLYCOO_CHUNK", "8192"))
     want = _cdiv(max(int(nnz), 1), 148 * 4)
-    return int(min(8192, max(tile, _cdiv(want, tile) * tile)))
+    return int(min(cap, max(tile, _cdiv(want, tile) * tile)))
 
 
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None) -> ModeWork:
