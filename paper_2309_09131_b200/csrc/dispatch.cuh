@@ -1,7 +1,8 @@
 // Fast-path dispatch: (N, mode, R) -> kernel instance.  The one-CTA-per-chunk
-// tile kernel (fast_kernel.cuh) is the default; FLYCOO_KERNEL=pipe selects the
-// persistent warp-specialised pipeline (pipe_kernel.cuh) for A/B runs
-// (round 1: 5.50 vs 5.18 ms per c2 sweep, the tile kernel wins).
+// tile kernel (fast_kernel.cuh) is the default; FLYCOO_KERNEL=pipe|warp select
+// the persistent warp-specialised pipeline (pipe_kernel.cuh) or the
+// warp-independent kernel (warp_kernel.cuh) for A/B runs -- both slower in
+// round 1 (profiles/r1_kernel_experiments.md).
 #pragma once
 
 #include <stdlib.h>
@@ -12,13 +13,13 @@
 
 namespace fc {
 
-// 0 = warp-independent (default), 1 = tile, 2 = pipeline
+// 1 = tile (default), 0 = warp-independent, 2 = pipeline (FLYCOO_KERNEL=warp|pipe)
 inline int kernel_kind() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("FLYCOO_KERNEL");
-    v = 0;
-    if (e && strcmp(e, "tile") == 0) v = 1;
+    v = 1;
+    if (e && strcmp(e, "warp") == 0) v = 0;
     if (e && strcmp(e, "pipe") == 0) v = 2;
   }
   return v;
