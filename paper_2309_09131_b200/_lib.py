@@ -31,12 +31,13 @@ _SIGS = {
     "fc_value_embedded": (_int, [_int]),
     "fc_smem_acc_rows_max": (_i64, [_int]),
     "fc_tile_elems": (_int, []),
+    "fc_chunk_rows_max": (_i64, [_int, _int, _i64]),
     "fc_mode_worker": (_int, [
         _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val
         _vp, _vp,                      # factors (host array of device ptrs), out
         _int, _int, _int,              # nmodes, mode, rank
         _i64, _i64,                    # out_rows, m_mode
-        _vp, _vp, _vp, _i64,           # chunk_start, chunk_ss, chunk_part, nchunks
+        _vp, _vp, _vp, _vp, _i64, _i64,  # chunk_start, chunk_ss, chunk_part, chunk_rows, tile_rows, nchunks
         _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
         _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots, nnz
         _int, _int, _int,              # do_compute, do_remap, acc_in_smem

@@ -114,13 +114,13 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const int hstride = (int)((a.m + 3) / 4 * 4);
+  const int hstride = (int)((a.tile_rows + 3) / 4 * 4);
   int4 *s_sorted = reinterpret_cast<int4 *>(smem);
   float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
   int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
   unsigned char *tail = smem + FP::fixed_bytes;
   int *s_hist = reinterpret_cast<int *>(tail);
-  tail += FP::hist_bytes(a.m);
+  tail += FP::hist_bytes(a.tile_rows);
   int *s_bnd_row = reinterpret_cast<int *>(tail);
   tail += 2 * G * sizeof(int);
   float *s_bnd = reinterpret_cast<float *>(tail);
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   const int64_t ss = a.chunk_ss[chunk];
   const int part = a.chunk_part[chunk];
   const int64_t row0 = ss * a.m;
-  const int rows = (int)min64(a.m, a.out_rows - row0);
+  const int rows = chunk_row_count(a, chunk, row0);
   const int irow0 = (int)row0;
 
   for (int i = tid; i < rows * R; i += kFBlock) s_acc[i] = 0.f;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.m);
+  const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.tile_rows);
   auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT>;
   static size_t configured = 0;
   if (smem > configured) {

@@ -22,6 +22,8 @@ struct ModeArgs {
   const int64_t *chunk_start;
   const int32_t *chunk_ss;
   const int32_t *chunk_part;
+  const int32_t *chunk_rows;  // rows of a chunk merging several small super-shards (or null)
+  int64_t tile_rows;          // max rows of any chunk (accumulator tile height, >= m)
   float *part_ws;
   const uint32_t *slots;
   int64_t nnz;
@@ -29,6 +31,13 @@ struct ModeArgs {
   int32_t *flags;
   unsigned long long *counters;
 };
+
+// Output rows [row0, row0 + rows) owned by chunk c: its first super-shard's
+// row offset, and either one super-shard's rows or the merged row count.
+__device__ __forceinline__ int chunk_row_count(const ModeArgs &a, int64_t c, int64_t row0) {
+  const int64_t r = a.chunk_rows ? (int64_t)a.chunk_rows[c] : a.m;
+  return (int)min64(r, a.out_rows - row0);
+}
 
 __device__ __forceinline__ int4 ld_stream_v4(const int4 *p) {
   int4 r;

@@ -81,12 +81,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const int hstride = (int)((a.m + 3) / 4 * 4);
+  const int hstride = (int)((a.tile_rows + 3) / 4 * 4);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + 2 * PP::buf_bytes);
   int *s_pmisc = reinterpret_cast<int *>(smem + 2 * PP::buf_bytes + 2 * sizeof(TileMeta));
   unsigned char *tail = smem + PP::fixed_bytes;
   int *s_hist = reinterpret_cast<int *>(tail);
-  tail += PP::hist_bytes(a.m);
+  tail += PP::hist_bytes(a.tile_rows);
   int *s_bnd_row = reinterpret_cast<int *>(tail);
   tail += 2 * G * sizeof(int);
   float *s_bnd = reinterpret_cast<float *>(tail);
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
       const int64_t start = a.chunk_start[chunk];
       const int64_t end = a.chunk_start[chunk + 1];
       const int64_t row0 = a.chunk_ss[chunk] * a.m;
-      const int rows = (int)min64(a.m, a.out_rows - row0);
+      const int rows = chunk_row_count(a, chunk, row0);
       const int irow0 = (int)row0;
       auto key_of = [&](const int4 &r) {
         const int lr = comp<MODE>(r) - irow0;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
       if (meta.chunk < 0) break;
       const int64_t chunk = meta.chunk;
       const int64_t row0 = a.chunk_ss[chunk] * a.m;
-      const int rows = (int)min64(a.m, a.out_rows - row0);
+      const int rows = chunk_row_count(a, chunk, row0);
       const int irow0 = (int)row0;
       if (meta.first) {
         for (int i = ctid; i < rows * R; i += kConsThreads) s_acc[i] = 0.f;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_pipe(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = PipePlan<NM, LPG>::total(a.rank, a.m);
+  const size_t smem = PipePlan<NM, LPG>::total(a.rank, a.tile_rows);
   auto kern = mode_pass_pipe_kernel<NM, MODE, LPG, RT>;
   static size_t configured = 0;
   if (smem > configured) {

@@ -64,15 +64,15 @@ __global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const Mod
   const unsigned lt_mask = (1u << lane) - 1u;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const size_t wbytes = WP::per_warp(R, a.m);
+  const size_t wbytes = WP::per_warp(R, a.tile_rows);
   auto warp_base = [&](int w) { return smem + w * wbytes; };
   unsigned char *base = warp_base(warp);
   int4 *s_sorted = reinterpret_cast<int4 *>(base);
   float *s_sval = reinterpret_cast<float *>(base + WP::sorted_bytes);
   int *s_hist = reinterpret_cast<int *>(base + WP::off_hist());
-  int *s_bnd_row = reinterpret_cast<int *>(base + WP::off_brow(a.m));
-  float *s_bnd = reinterpret_cast<float *>(base + WP::off_bnd(a.m));
-  const size_t acc_off = WP::off_acc(R, a.m);
+  int *s_bnd_row = reinterpret_cast<int *>(base + WP::off_brow(a.tile_rows));
+  float *s_bnd = reinterpret_cast<float *>(base + WP::off_bnd(a.tile_rows));
+  const size_t acc_off = WP::off_acc(R, a.tile_rows);
   float *s_acc = reinterpret_cast<float *>(base + acc_off);
 
   const int64_t chunk = blockIdx.x;
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const Mod
   const int64_t ss = a.chunk_ss[chunk];
   const int part = a.chunk_part[chunk];
   const int64_t row0 = ss * a.m;
-  const int rows = (int)min64(a.m, a.out_rows - row0);
+  const int rows = chunk_row_count(a, chunk, row0);
   const int irow0 = (int)row0;
 
   for (int i = lane; i < rows * R; i += 32) s_acc[i] = 0.f;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const Mod
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_warp(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = WarpPlan<NM, LPG>::total(a.rank, a.m);
+  const size_t smem = WarpPlan<NM, LPG>::total(a.rank, a.tile_rows);
   auto kern = mode_pass_warp_kernel<NM, MODE, LPG, RT>;
   static size_t configured = 0;
   if (smem > configured) {

@@ -232,7 +232,9 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
         _lib.call("fc_mode_worker", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
                   val_p(st.val[b]), fptrs, out.data_ptr(), nmodes, mode, rank, dims[mode],
                   params.m[mode], work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),
-                  work.chunk_part.data_ptr(), work.nchunks, work.red1.data_ptr(), work.nred1,
+                  work.chunk_part.data_ptr(),
+                  work.chunk_rows.data_ptr() if work.chunk_rows is not None else None,
+                  work.tile_rows, work.nchunks, work.red1.data_ptr(), work.nred1,
                   work.red2.data_ptr(), work.nred2,
                   work.part_ws.data_ptr() if work.part_ws is not None else None,
                   work.part_ws2.data_ptr() if work.part_ws2 is not None else None,

@@ -77,7 +77,8 @@ def _worker(rank, world, port, result):
                 p = dt.plans[(n + 1) % N]
                 got, gval = dt.local_records()
                 assert torch.equal(got, ref_st.crd[ref_st.active][p.e_lo:p.e_hi]), (rank, N, n)
-                assert torch.equal(working[n], ref_out), (rank, N, n)
+                # merged-chunk grouping may differ at rank boundaries: fp32 reassociation only
+                assert torch.allclose(working[n], ref_out, rtol=1e-5, atol=0), (rank, N, n)
             ops.check(dt)
         result[rank] = 1
     finally:

@@ -266,7 +266,8 @@ def test_injected_faults_raise():
     with pytest.raises(ShardOverflowError):
         mttkrp_mode(st, fs, 0, smap)
     st = build_device_sharded(z["subs"], z["vals"], params)
-    st.crd[0][0, 0] = int(z["dims"][0]) - 1 if int(st.crd[0][0, 0]) < params.m[0] else 0
+    # an output coordinate outside every super-shard row range of the chunk
+    st.crd[0][0, 0] = int(z["dims"][0]) + 3
     with pytest.raises(BufferOrderError):
         mttkrp_mode(st, fs, 0, smap)
 

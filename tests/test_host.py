@@ -77,7 +77,7 @@ def test_mode_work_partitions_elements():
                           minlength=params.k[n]) for n, d in enumerate(params.dims)]
     plan = plan_from_counts(params, counts)
     for n in range(3):
-        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=2048)
+        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=2048, merge=False)
         cs = w.chunk_start.numpy()
         assert cs[0] == 0 and cs[-1] == plan.nnz and np.all(np.diff(cs) > 0)
         ss = w.chunk_ss.numpy()
@@ -100,3 +100,45 @@ def test_mode_work_partitions_elements():
                 assert (t1[:, 3] >= 0).all()
                 t2 = r2[r2[:, 0] == s_]
                 assert len(t2) == 1 and list(range(t2[0, 1], t2[0, 2])) == sorted(t1[:, 3].tolist())
+
+
+def test_mode_work_merges_small_super_shards():
+    """With merging, chunks partition the elements, every output row is owned
+    by exactly one writer (a chunk or a reduce task), and merged chunks hold
+    only whole super-shards within the row capacity."""
+    rng = np.random.default_rng(1)
+    dims = (200000, 300, 50)
+    params = device_params(dims, 100_000, 32)
+    counts = [np.bincount(np.minimum(rng.zipf(1.3, 100_000) - 1, d - 1) // params.m[n],
+                          minlength=params.k[n]) for n, d in enumerate(dims)]
+    plan = plan_from_counts(params, counts)
+    L = _lib.load()
+    for n in range(3):
+        w = make_mode_work(plan, n, 32, "cpu", chunk_elems=4096)
+        m = params.m[n]
+        cs = w.chunk_start.numpy()
+        assert cs[0] == 0 and cs[-1] == plan.nnz and np.all(np.diff(cs) >= 0)
+        ss = w.chunk_ss.numpy().astype(np.int64)
+        part = w.chunk_part.numpy()
+        offs = plan.ss_elem_offsets[n]
+        owner = np.zeros(dims[n], dtype=np.int64)
+        if w.chunk_rows is None:
+            rows = np.minimum(m, dims[n] - ss * m)
+        else:
+            rows = w.chunk_rows.numpy().astype(np.int64)
+            assert w.tile_rows == L.fc_chunk_rows_max(3, 32, m) and rows.max() <= w.tile_rows
+            assert plan.nnz < 2048 * params.k[n]  # only sparse modes merge
+        for c in range(w.nchunks):
+            nss = -(-rows[c] // m)
+            assert cs[c] >= offs[ss[c]] and cs[c + 1] <= offs[ss[c] + nss]
+            if part[c] < 0:
+                owner[ss[c] * m: ss[c] * m + rows[c]] += 1
+        for s_, p0, p1, dst in w.red1.numpy():
+            if dst < 0:
+                owner[s_ * m: min((s_ + 1) * m, dims[n])] += 1
+        for s_, q0, q1 in w.red2.numpy():
+            owner[s_ * m: min((s_ + 1) * m, dims[n])] += 1
+        assert np.all(owner == 1), n
+    # the sparse first mode actually merges
+    w0 = make_mode_work(plan, 0, 32, "cpu", chunk_elems=4096)
+    assert w0.chunk_rows is not None and int(w0.chunk_rows.max()) > params.m[0]
