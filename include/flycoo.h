@@ -59,8 +59,8 @@ const char *fc_last_error(void);
  * shared memory; larger intervals accumulate in global memory (out rows). */
 int64_t fc_smem_acc_rows_max(int rank);
 int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
-/* Row capacity of one chunk when consecutive small super-shards are merged
- * into it (fast path only; returns m when merging is not supported). */
+/* Row capacity of a "direct" chunk merging consecutive small super-shards
+ * (fast path only; returns m when merging is not supported). */
 int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);
 
 /* ------------------------------------------------------------------ K1/K2
@@ -76,7 +76,9 @@ int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);
  *   chunk_rows (optional, fast path): a chunk may cover several whole
  *   consecutive super-shards starting at chunk_ss[c]; it then owns
  *   chunk_rows[c] rows (<= tile_rows <= fc_chunk_rows_max) and chunk_part[c]
- *   is -1.
+ *   is -1; or, with chunk_part[c] == -2 ("direct"), at most one tile
+ *   (fc_tile_elems) of nonzeros and chunk_rows[c] <= hist_rows <= 256 rows,
+ *   stored straight to `out` without an accumulator tile.
  *   Deterministic two-level reduce of the partials (K2): red1 holds nred1
  *   tasks {ss, p0, p1, dst}: rows of super-shard ss = sum of partials
  *   [p0, p1) in chunk order, written to `out` (dst < 0) or to part_ws2 slot
@@ -95,7 +97,7 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
                    int64_t out_rows, int64_t m_mode,
                    const int64_t *chunk_start, const int32_t *chunk_ss,
                    const int32_t *chunk_part, const int32_t *chunk_rows,
-                   int64_t tile_rows, int64_t nchunks,
+                   int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
                    const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
                    float *part_ws, float *part_ws2, const uint32_t *dest_slots, int64_t nnz,
                    int do_compute, int do_remap, int acc_in_smem,

@@ -37,7 +37,7 @@ _SIGS = {
         _vp, _vp,                      # factors (host array of device ptrs), out
         _int, _int, _int,              # nmodes, mode, rank
         _i64, _i64,                    # out_rows, m_mode
-        _vp, _vp, _vp, _vp, _i64, _i64,  # chunk_start, chunk_ss, chunk_part, chunk_rows, tile_rows, nchunks
+        _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks
         _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
         _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots, nnz
         _int, _int, _int,              # do_compute, do_remap, acc_in_smem

@@ -27,6 +27,8 @@ inline int kernel_kind() {
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  // direct chunks (hist_rows > tile_rows) exist only in the tile kernel
+  if (a.hist_rows > a.tile_rows) return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
   switch (kernel_kind()) {
     case 1: return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
     case 2: return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);

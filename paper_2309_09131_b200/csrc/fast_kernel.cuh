@@ -50,8 +50,8 @@ struct FastPlan {
   // dynamic tail: per-warp row histograms (m ints each), boundary entries,
   // the m x R accumulator tile
   __host__ __device__ static size_t hist_bytes(int64_t m) { return sizeof(int) * kFWarps * ((m + 3) / 4 * 4); }
-  static size_t total(int rank, int64_t m) {
-    return fixed_bytes + hist_bytes(m) + (size_t)2 * G * sizeof(int) +
+  static size_t total(int rank, int64_t m, int64_t hist_rows = 0) {
+    return fixed_bytes + hist_bytes(hist_rows > m ? hist_rows : m) + (size_t)2 * G * sizeof(int) +
            (size_t)2 * G * rank * sizeof(float) + (size_t)m * rank * sizeof(float);
   }
 };
@@ -114,13 +114,13 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const int hstride = (int)((a.tile_rows + 3) / 4 * 4);
+  const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
   int4 *s_sorted = reinterpret_cast<int4 *>(smem);
   float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
   int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
   unsigned char *tail = smem + FP::fixed_bytes;
   int *s_hist = reinterpret_cast<int *>(tail);
-  tail += FP::hist_bytes(a.tile_rows);
+  tail += FP::hist_bytes(a.hist_rows);
   int *s_bnd_row = reinterpret_cast<int *>(tail);
   tail += 2 * G * sizeof(int);
   float *s_bnd = reinterpret_cast<float *>(tail);
@@ -139,7 +139,19 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   const int rows = chunk_row_count(a, chunk, row0);
   const int irow0 = (int)row0;
 
-  for (int i = tid; i < rows * R; i += kFBlock) s_acc[i] = 0.f;
+  // direct chunk (part == -2): whole super-shards in <= one tile; every row is
+  // complete inside the tile and is stored straight to `out` (no tile acc)
+  const bool direct = part == kPartDirect;
+  float *out_rows = a.out + row0 * R;
+  if (direct) {
+    if (start == end) {  // only empty super-shards: their rows are zero
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = tid; i < rows * R / 4; i += kFBlock) reinterpret_cast<float4 *>(out_rows)[i] = z;
+      return;
+    }
+  } else {
+    for (int i = tid; i < rows * R; i += kFBlock) s_acc[i] = 0.f;
+  }
 
   const int gi = tid / LPG;
   const int lg = tid % LPG;
@@ -230,6 +242,10 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       if (tid < rows) {
 #pragma unroll 4
         for (int w = 0; w < kFWarps; ++w) tot += s_hist[w * hstride + tid];
+        if (direct && tot == 0) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
+        }
       }
       int incl = tot;
 #pragma unroll
@@ -303,6 +319,10 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
           if (lg == 0) s_bnd_row[2 * gi] = cur - irow0;
           if (col_ok) VecT<4>::store(s_bnd + (2 * gi) * R + col, acc);
         } else if (col_ok) {
+          if (direct) {  // the whole row is this segment
+            VecT<4>::store(out_rows + (cur - irow0) * R + col, acc);
+            return;
+          }
           float *p = s_acc + (cur - irow0) * R + col;
           float o[4];
           VecT<4>::load(p, o);
@@ -443,19 +463,22 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
               run += x3;
             }
             for (; e < e3; ++e) run += s_bnd[e * R + c];
-            s_acc[row * R + c] += run;
+            if (direct) out_rows[row * R + c] = run;
+            else s_acc[row * R + c] += run;
           }
         }
       }
     }
     FAST_PROBE(4);
   }
-  __syncthreads();
-  float *dstp = part < 0 ? a.out + row0 * R : a.part_ws + (int64_t)part * a.m * R;
-  const int n4 = rows * R / 4;
-  const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
-  float4 *d4 = reinterpret_cast<float4 *>(dstp);
-  for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
+  if (!direct) {
+    __syncthreads();
+    float *dstp = part < 0 ? out_rows : a.part_ws + (int64_t)part * a.m * R;
+    const int n4 = rows * R / 4;
+    const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
+    float4 *d4 = reinterpret_cast<float4 *>(dstp);
+    for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
+  }
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 #ifdef FAST_PHASE_TIMING
   if (tid == 0)
@@ -465,7 +488,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 
 template <int NM, int MODE, int LPG, int RT>
 int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.tile_rows);
+  const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.tile_rows, a.hist_rows);
   auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT>;
   static size_t configured = 0;
   if (smem > configured) {

@@ -23,7 +23,8 @@ struct ModeArgs {
   const int32_t *chunk_ss;
   const int32_t *chunk_part;
   const int32_t *chunk_rows;  // rows of a chunk merging several small super-shards (or null)
-  int64_t tile_rows;          // max rows of any chunk (accumulator tile height, >= m)
+  int64_t tile_rows;          // accumulator tile height (>= m): max rows of non-direct chunks
+  int64_t hist_rows;          // max rows of any chunk (counting-sort bins, <= 256)
   float *part_ws;
   const uint32_t *slots;
   int64_t nnz;
@@ -31,6 +32,10 @@ struct ModeArgs {
   int32_t *flags;
   unsigned long long *counters;
 };
+
+// chunk_part value of a direct chunk: whole super-shards within one tile,
+// rows stored straight to `out` (fast tile kernel only)
+constexpr int kPartDirect = -2;
 
 // Output rows [row0, row0 + rows) owned by chunk c: its first super-shard's
 // row offset, and either one super-shard's rows or the merged row count.

@@ -440,7 +440,7 @@ int launch_mode_pass(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
 // Fast path when the accumulator tile is in shared memory, m <= 256,
 // N <= 4 and R % 4 == 0, R <= 64; the general kernel otherwise.
 bool fast_ok(const ModeArgs &a, bool smem_acc) {
-  return smem_acc && a.tile_rows <= kMaxBins && a.nmodes >= 2 && a.nmodes <= 4 && a.rank % 4 == 0 &&
+  return smem_acc && a.hist_rows <= kMaxBins && a.nmodes >= 2 && a.nmodes <= 4 && a.rank % 4 == 0 &&
          a.rank <= 64;
 }
 
@@ -472,30 +472,24 @@ using namespace fc;
 extern "C" {
 
 int64_t fc_smem_acc_rows_max(int rank) { return fc::smem_acc_rows_max(rank); }
-
-// Row capacity of a merged chunk on the fast path: the largest multiple of m
-// (<= 256 rows, the counting-sort bins) whose accumulator tile keeps the
-// tile kernel at 3 CTAs per SM; m when super-shards cannot be merged.
-int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m) {
-  if (m < 1 || m > kMaxBins || nmodes < 2 || nmodes > 4 || rank % 4 != 0 || rank > 64) return m;
-  // shared bytes of the tile kernel (fast_kernel.cuh FastPlan), 3 CTAs/SM
-  const int lpg = rank == 16 ? 4 : rank == 32 ? 8 : 16;
-  const int64_t G = kBlock / lpg, tile = 2048;
-  const int64_t fixed = 16 * (tile + G) + (nmodes == 4 ? 4 * (tile + G) : 0) + 64 + 8 * G +
-                        8 * G * rank;
-  const int64_t limit = 227 * 1024 / 3 - 1024;
-  int64_t rows = m;
-  while (rows + m <= kMaxBins && fixed + (rows + m) * (4 * kWarps + 4 * (int64_t)rank) <= limit)
-    rows += m;
-  return rows;
-}
 int fc_tile_elems(void) { return kTile; }
+
+// Row capacity of a direct chunk (several whole super-shards in at most one
+// tile, rows stored straight to `out`): the largest multiple of m within the
+// 256 counting-sort bins on the fast path; m when merging is not supported.
+int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m) {
+  if (m < 1 || m > kMaxBins || nmodes < 2 || nmodes > 4 || rank % 4 != 0 || rank > 64 ||
+      m > smem_acc_rows_max(rank))
+    return m;
+  return kMaxBins / m * m;
+}
 
 int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
                    const float *const *factors, float *out, int nmodes, int mode, int rank,
                    int64_t out_rows, int64_t m_mode, const int64_t *chunk_start,
                    const int32_t *chunk_ss, const int32_t *chunk_part,
-                   const int32_t *chunk_rows, int64_t tile_rows, int64_t nchunks,
+                   const int32_t *chunk_rows, int64_t tile_rows, int64_t hist_rows,
+                   int64_t nchunks,
                    const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
                    float *part_ws, float *part_ws2, const uint32_t *dest_slots, int64_t nnz,
                    int do_compute,
@@ -535,9 +529,10 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
   FC_CHECK_ARG(!acc_in_smem || m_mode <= smem_acc_rows_max(rank),
                "m=%lld too large for shared-memory accumulation at rank %d", (long long)m_mode, rank);
   FC_CHECK_ARG(m_mode < (1ll << 30), "interval width too large");
-  FC_CHECK_ARG(!chunk_rows || (acc_in_smem && tile_rows >= m_mode &&
-                               tile_rows <= fc_chunk_rows_max(nmodes, rank, m_mode)),
-               "merged chunks need the fast path and tile_rows in [m, fc_chunk_rows_max]");
+  FC_CHECK_ARG(!chunk_rows || (acc_in_smem && tile_rows >= m_mode && tile_rows <= kMaxBins &&
+                               hist_rows <= fc_chunk_rows_max(nmodes, rank, m_mode)),
+               "merged chunks need the fast path, tile_rows in [m, 256] and hist_rows <= "
+               "fc_chunk_rows_max");
   ModeArgs a{};
   a.src = static_cast<const int4 *>(src_crd);
   a.src_val = src_val;
@@ -558,6 +553,7 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
   a.chunk_part = chunk_part;
   a.chunk_rows = chunk_rows;
   a.tile_rows = chunk_rows ? tile_rows : m_mode;
+  a.hist_rows = chunk_rows ? (hist_rows > a.tile_rows ? hist_rows : a.tile_rows) : m_mode;
   a.part_ws = part_ws;
   a.slots = dest_slots;
   a.nnz = nnz;

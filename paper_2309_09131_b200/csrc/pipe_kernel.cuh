@@ -81,12 +81,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
   const int R = RT > 0 ? RT : a.rank;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  const int hstride = (int)((a.tile_rows + 3) / 4 * 4);
+  const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + 2 * PP::buf_bytes);
   int *s_pmisc = reinterpret_cast<int *>(smem + 2 * PP::buf_bytes + 2 * sizeof(TileMeta));
   unsigned char *tail = smem + PP::fixed_bytes;
   int *s_hist = reinterpret_cast<int *>(tail);
-  tail += PP::hist_bytes(a.tile_rows);
+  tail += PP::hist_bytes(a.hist_rows);
   int *s_bnd_row = reinterpret_cast<int *>(tail);
   tail += 2 * G * sizeof(int);
   float *s_bnd = reinterpret_cast<float *>(tail);

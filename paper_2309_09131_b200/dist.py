@@ -225,7 +225,7 @@ class CudaOps:
                   vp(dt.val[b]), fptrs, out.data_ptr(), dt.num_modes, mode, R, params.dims[mode],
                   params.m[mode], w.chunk_start.data_ptr(), w.chunk_ss.data_ptr(),
                   w.chunk_part.data_ptr(),
-                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.nchunks, w.red1.data_ptr(), w.nred1, w.red2.data_ptr(),
+                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(), w.nred1, w.red2.data_ptr(),
                   w.nred2, vp(w.part_ws), vp(w.part_ws2), p.local_slots.data_ptr(),
                   dt.cap + p.send_total, 1, 1, int(w.acc_in_smem), flags_p, proc_p,
                   torch.cuda.current_stream().cuda_stream)

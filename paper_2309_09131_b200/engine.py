@@ -234,7 +234,7 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
                   params.m[mode], work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),
                   work.chunk_part.data_ptr(),
                   work.chunk_rows.data_ptr() if work.chunk_rows is not None else None,
-                  work.tile_rows, work.nchunks, work.red1.data_ptr(), work.nred1,
+                  work.tile_rows, work.hist_rows, work.nchunks, work.red1.data_ptr(), work.nred1,
                   work.red2.data_ptr(), work.nred2,
                   work.part_ws.data_ptr() if work.part_ws is not None else None,
                   work.part_ws2.data_ptr() if work.part_ws2 is not None else None,

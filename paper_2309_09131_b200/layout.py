@@ -111,7 +111,8 @@ class ModeWork:
     chunk_ss: torch.Tensor      # int32
     chunk_part: torch.Tensor    # int32
     chunk_rows: torch.Tensor | None  # int32 rows per chunk when small super-shards are merged
-    tile_rows: int              # max rows of a chunk (>= m)
+    tile_rows: int              # accumulator tile height (m)
+    hist_rows: int              # max rows of any chunk (direct chunks: <= 256)
     red1: torch.Tensor          # int64 (nred1, 4): ss, p0, p1, dst
     nred1: int
     red2: torch.Tensor          # int64 (nred2, 3): ss, q0, q1
@@ -159,34 +160,31 @@ def default_chunk_elems(nnz: int, tile: int = 2048) -> int:
     return int(min(cap, max(tile, _cdiv(want, tile) * tile)))
 
 
-def merge_small_super_shards(counts: np.ndarray, C: int, group: int):
-    """Greedy grouping of consecutive super-shards into chunks: a super-shard
-    with >= C/2 nonzeros gets its own chunk(s) (C-element pieces); smaller
-    ones (empty ones included) are packed, at most `group` of them and at
-    most C nonzeros per chunk.  Returns (first_ss, n_ss, n_pieces) per chunk
-    group; n_pieces > 1 only for a single big super-shard."""
-    first, nss, pieces = [], [], []
+PART_DIRECT = -2  # chunk_part of a direct chunk (see fc_mode_worker)
+
+
+def direct_groups(counts: np.ndarray, tile: int, group: int):
+    """Greedy packing of consecutive super-shards into direct chunks: at most
+    `group` super-shards and at most one tile of nonzeros each (empty
+    super-shards included).  Super-shards larger than a tile are left alone
+    (n_ss = 0 marks them).  Returns (first_ss, n_ss) per chunk group."""
+    first, nss = [], []
     k = counts.shape[0]
     i = 0
-    half = max(C // 2, 1)
     while i < k:
-        c = int(counts[i])
-        if c >= half:
+        if int(counts[i]) > tile:
             first.append(i)
-            nss.append(1)
-            pieces.append(-(-c // C))
+            nss.append(0)
             i += 1
             continue
         j, tot = i, 0
-        while j < k and j - i < group and int(counts[j]) < half and tot + int(counts[j]) <= C:
+        while j < k and j - i < group and tot + int(counts[j]) <= tile:
             tot += int(counts[j])
             j += 1
         first.append(i)
         nss.append(j - i)
-        pieces.append(1)
         i = j
-    return (np.asarray(first, dtype=np.int64), np.asarray(nss, dtype=np.int64),
-            np.asarray(pieces, dtype=np.int64))
+    return np.asarray(first, dtype=np.int64), np.asarray(nss, dtype=np.int64)
 
 
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None,
@@ -208,39 +206,39 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
     smem = m <= int(L.fc_smem_acc_rows_max(int(rank)))
     dev = torch.device(device)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    # Merging costs shared memory (a taller accumulator tile for EVERY chunk of
-    # the launch, i.e. less L1 for factor rows), so it is used only for sparse
-    # modes whose super-shards average less than one tile of nonzeros.
+    # Sparse modes (super-shards average less than one tile of nonzeros):
+    # consecutive small super-shards become "direct" chunks -- whole rows in
+    # one tile, stored straight to `out` -- instead of one tiny chunk each.
     sparse = nnz < tile * max(k, 1)
-    tile_rows = (int(L.fc_chunk_rows_max(params.num_modes, int(rank), m))
-                 if (smem and merge and sparse) else m)
-    group = max(tile_rows // m, 1)
+    rows_cap = int(L.fc_chunk_rows_max(params.num_modes, int(rank), m)) if smem else m
+    group = rows_cap // m if (merge and sparse) else 1
     if smem and group > 1:
         C = int(chunk_elems or default_chunk_elems(nnz, tile))
-        first, nss, pieces = merge_small_super_shards(counts, C, group)
+        first, nss = direct_groups(counts, tile, group)
+        big = nss == 0
+        pieces = np.where(big, -(-counts[first] // C), 1)
         total = int(pieces.sum())
         grp_of = np.repeat(np.arange(first.shape[0], dtype=np.int64), pieces)
-        grp_first_chunk = np.concatenate(([0], np.cumsum(pieces)))[:-1]
-        j = np.arange(total, dtype=np.int64) - grp_first_chunk[grp_of]
+        j = np.arange(total, dtype=np.int64) - np.concatenate(([0], np.cumsum(pieces)))[:-1][grp_of]
         ss_of = first[grp_of]
         starts = offs[ss_of] + j * C
         chunk_start = np.concatenate((starts, [nnz])).astype(np.int64)
-        dims_m = params.dims[mode]
-        rows = np.minimum(nss[grp_of] * m, dims_m - ss_of * m).astype(np.int32)
-        # partial tiles only for big super-shards split into several pieces
-        nch_ss = np.zeros(k, dtype=np.int64)
-        nch_ss[first] = np.where(pieces > 1, pieces, 0)
+        rows = np.minimum(np.where(big[grp_of], 1, nss[grp_of]) * m,
+                          params.dims[mode] - ss_of * m).astype(np.int32)
+        nch_ss = np.ones(k, dtype=np.int64)
+        nch_ss[first[big]] = pieces[big]
         multi = nch_ss >= 2
         part_base = np.concatenate(([0], np.cumsum(np.where(multi, nch_ss, 0))))
-        part = np.where(multi[ss_of], part_base[:-1][ss_of] + j, -1).astype(np.int32)
+        part = np.where(big[grp_of],
+                        np.where(multi[ss_of], part_base[:-1][ss_of] + j, -1),
+                        PART_DIRECT).astype(np.int32)
         nparts = int(part_base[-1])
-        # every super-shard is covered by a chunk, so only split ones reduce
-        r1, r2, nslots = reduce_plan(np.where(multi, nch_ss, 1), part_base)
+        r1, r2, nslots = reduce_plan(nch_ss, part_base)
         ws = torch.empty(nparts * m * rank, dtype=torch.float32, device=dev) if nparts else None
         ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
         return ModeWork(True, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), t(rows),
-                        int(tile_rows), t(r1), int(r1.shape[0]), t(r2), int(r2.shape[0]), nparts, ws,
-                        ws2, C)
+                        m, int(rows.max()) if rows.size else m, t(r1), int(r1.shape[0]), t(r2),
+                        int(r2.shape[0]), nparts, ws, ws2, C)
     if smem:
         if chunk_elems is None:
             chunk_elems = default_chunk_elems(nnz, tile)
@@ -268,7 +266,7 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
         r2 = np.zeros((0, 3), dtype=np.int64)
     ws = torch.empty(nparts * m * rank, dtype=torch.float32, device=dev) if nparts else None
     ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
-    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), None, m,
+    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), None, m, m,
                     t(r1), int(r1.shape[0]), t(r2), int(r2.shape[0]), nparts, ws, ws2, C)
 
 

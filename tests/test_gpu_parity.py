@@ -310,3 +310,28 @@ def test_c2_sample_vs_oracle_and_full_cycle():
                    what=f"c2 sample mode {n}")
     end = host_records(st)
     assert np.array_equal(start[0], end[0]) and np.array_equal(start[1], end[1])
+
+
+def test_sparse_mode_direct_chunks():
+    """A mode with far more rows than nonzeros per super-shard: consecutive
+    super-shards are packed into direct chunks (rows stored straight to
+    `out`, empty rows zeroed); parity with the oracle, including empty rows."""
+    from paper_2309_09131_b200.layout import PART_DIRECT
+    rng = np.random.default_rng(8)
+    dims = (300000, 400, 60)
+    draws = np.column_stack([np.minimum(rng.zipf(1.2, 300_000) - 1, dims[0] - 1),
+                             rng.integers(0, dims[1], 300_000), rng.integers(0, dims[2], 300_000)])
+    _, first = np.unique(draws, axis=0, return_index=True)
+    subs = draws[np.sort(first)][:200_000]
+    vals = rng.uniform(0.1, 1.0, len(subs)).astype(np.float32).astype(np.float64)
+    for rank in (16, 32):
+        params = device_params(dims, len(vals), rank)
+        st = build_device_sharded(subs, vals, params)
+        smap = schedule_super_shards(st.plan, 1)
+        w = st.mode_work(0, rank)
+        assert (w.chunk_part.cpu().numpy() == PART_DIRECT).any()
+        fs = factors_f32(dims, rank, 5)
+        for n in range(3):
+            out = mttkrp_mode(st, DeviceFactorSet.from_host(fs), n, smap)
+            assert_rel(out.double().cpu().numpy(), oracle.reference_mttkrp(subs, vals, fs, n),
+                       what=f"direct R={rank} mode {n}")

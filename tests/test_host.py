@@ -103,9 +103,10 @@ def test_mode_work_partitions_elements():
 
 
 def test_mode_work_merges_small_super_shards():
-    """With merging, chunks partition the elements, every output row is owned
-    by exactly one writer (a chunk or a reduce task), and merged chunks hold
-    only whole super-shards within the row capacity."""
+    """Sparse modes: chunks partition the elements, every output row has
+    exactly one writer (a chunk or a reduce task), direct chunks hold whole
+    super-shards, at most one tile of nonzeros and <= fc_chunk_rows_max rows."""
+    from paper_2309_09131_b200.layout import PART_DIRECT
     rng = np.random.default_rng(1)
     dims = (200000, 300, 50)
     params = device_params(dims, 100_000, 32)
@@ -113,6 +114,7 @@ def test_mode_work_merges_small_super_shards():
                           minlength=params.k[n]) for n, d in enumerate(dims)]
     plan = plan_from_counts(params, counts)
     L = _lib.load()
+    tile = L.fc_tile_elems()
     for n in range(3):
         w = make_mode_work(plan, n, 32, "cpu", chunk_elems=4096)
         m = params.m[n]
@@ -122,15 +124,14 @@ def test_mode_work_merges_small_super_shards():
         part = w.chunk_part.numpy()
         offs = plan.ss_elem_offsets[n]
         owner = np.zeros(dims[n], dtype=np.int64)
-        if w.chunk_rows is None:
-            rows = np.minimum(m, dims[n] - ss * m)
-        else:
-            rows = w.chunk_rows.numpy().astype(np.int64)
-            assert w.tile_rows == L.fc_chunk_rows_max(3, 32, m) and rows.max() <= w.tile_rows
-            assert plan.nnz < 2048 * params.k[n]  # only sparse modes merge
+        rows = (np.minimum(m, dims[n] - ss * m) if w.chunk_rows is None
+                else w.chunk_rows.numpy().astype(np.int64))
         for c in range(w.nchunks):
             nss = -(-rows[c] // m)
             assert cs[c] >= offs[ss[c]] and cs[c + 1] <= offs[ss[c] + nss]
+            if part[c] == PART_DIRECT:
+                assert cs[c + 1] - cs[c] <= tile and rows[c] <= L.fc_chunk_rows_max(3, 32, m)
+                assert cs[c] == offs[ss[c]] and cs[c + 1] == offs[ss[c] + nss]  # whole super-shards
             if part[c] < 0:
                 owner[ss[c] * m: ss[c] * m + rows[c]] += 1
         for s_, p0, p1, dst in w.red1.numpy():
@@ -139,6 +140,5 @@ def test_mode_work_merges_small_super_shards():
         for s_, q0, q1 in w.red2.numpy():
             owner[s_ * m: min((s_ + 1) * m, dims[n])] += 1
         assert np.all(owner == 1), n
-    # the sparse first mode actually merges
     w0 = make_mode_work(plan, 0, 32, "cpu", chunk_elems=4096)
-    assert w0.chunk_rows is not None and int(w0.chunk_rows.max()) > params.m[0]
+    assert (w0.chunk_part.numpy() == PART_DIRECT).any() and w0.hist_rows > params.m[0]

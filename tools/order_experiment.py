@@ -34,7 +34,7 @@ def timed(layout, mode, comp, remap, reps=5):
         _lib.call("fc_mode_worker", crd.data_ptr(), None, dst.data_ptr(), None, fptrs,
                   out.data_ptr(), N, mode, R, dims[mode], params.m[mode], w.chunk_start.data_ptr(),
                   w.chunk_ss.data_ptr(), w.chunk_part.data_ptr(),
-                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.nchunks, w.red1.data_ptr(),
+                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(),
                   w.nred1, w.red2.data_ptr(), w.nred2, vp(w.part_ws), vp(w.part_ws2),
                   slots.data_ptr(), nnz, comp, remap, int(w.acc_in_smem), flags_p, proc_p, strm)
     once()

@@ -31,7 +31,7 @@ def run(mode, comp, remap, reps=10):
         _lib.call("fc_mode_worker", st.crd[a].data_ptr(), None, st.crd[b].data_ptr(), None, fptrs,
                   out.data_ptr(), 3, mode, R, dims[mode], params.m[mode], w.chunk_start.data_ptr(),
                   w.chunk_ss.data_ptr(), w.chunk_part.data_ptr(),
-                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.nchunks, w.red1.data_ptr(),
+                  w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(),
                   w.nred1, w.red2.data_ptr(), w.nred2, vp(w.part_ws), vp(w.part_ws2),
                   st.slot_maps[mode].data_ptr(), st.nnz, comp, remap, int(w.acc_in_smem), flags_p,
                   proc_p, strm)
