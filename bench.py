@@ -355,6 +355,7 @@ def run_ours(args, rank, world, local):
                        f"dp{world}: per-mode super-shard row ranges, NCCL all_to_all_single remap + "
                        "all_gather_into_tensor of updated factor rows",
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
+                       "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
                        "mode_ms": [round(1e3 * x, 4) for x in mode_secs[:N]]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -125,8 +125,8 @@ int fc_scatter_records(const void *src_crd, const float *src_val, int64_t n,
  * (paper_2309_09131_b200/layout.py) sequences them.  `coords` is (nnz, N)
  * int32 in input order (seq), `ids` / `keys` are scratch of nnz entries. */
 /* Morton (hi, lo) of interval coordinates iv_w = coords[:, w] / m[w]
- * (morton.py:20-44); m/k are host arrays.  Returns FC_ERR_UNSUPPORTED if
- * the key needs more than 128 bits. */
+ * (morton.py:20-44); m/k are host arrays; hi may be NULL when the key fits
+ * 64 bits.  Returns FC_ERR_UNSUPPORTED if the key needs more than 128 bits. */
 int fc_build_morton(const int32_t *coords, int64_t nnz, int nmodes,
                     const int64_t *m, const int64_t *k,
                     uint64_t *hi, uint64_t *lo, void *stream);
@@ -161,6 +161,13 @@ int fc_build_invert(const uint32_t *order, int64_t nnz, uint32_t *pos, void *str
 /* slot[p] = pos_next[order[p]]  (layout.py:516-519 slot maps) */
 int fc_build_slots(const uint32_t *order, const uint32_t *pos_next, int64_t nnz,
                    uint32_t *slot, void *stream);
+/* Memory-lean forms used by the build: slot[pos_n[id]] = pos_next[id], and
+ * records scattered to their positions crd[pos[id]] = (coords[id], vals[id]). */
+int fc_build_slots_scatter(const uint32_t *pos_n, const uint32_t *pos_next, int64_t nnz,
+                           uint32_t *slot, void *stream);
+int fc_build_records_scatter(const uint32_t *pos, int64_t nnz, int nmodes,
+                             const int32_t *coords, const float *vals, void *crd,
+                             float *val_out, void *stream);
 /* Records of the active buffer in `order`: crd/val per the record layout. */
 int fc_build_records(const uint32_t *order, int64_t nnz, int nmodes,
                      const int32_t *coords, const float *vals, void *crd,

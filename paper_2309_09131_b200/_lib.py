@@ -54,6 +54,8 @@ _SIGS = {
     "fc_build_invert": (_int, [_vp, _i64, _vp, _vp]),
     "fc_build_slots": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "fc_build_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fc_build_slots_scatter": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "fc_build_records_scatter": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fc_synth_draw": (_int, [_c.c_uint64, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fc_synth_keys": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp]),
     "fc_synth_mark_first": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),

@@ -60,7 +60,7 @@ __global__ void morton_kernel(const int32_t *coords, int64_t nnz, MortonPlan mp,
         ++pos;
       }
     }
-    hi[i] = h;
+    if (hi) hi[i] = h;
     lo[i] = l;
   }
 }
@@ -137,6 +137,34 @@ __global__ void slots_kernel(const uint32_t *order, const uint32_t *pos_next, in
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x)
     slot[p] = pos_next[order[p]];
+}
+
+// slot[pos_n[id]] = pos_next[id]: the slot map from positions only (no orders)
+__global__ void slots_scatter_kernel(const uint32_t *pos_n, const uint32_t *pos_next, int64_t n,
+                                     uint32_t *slot) {
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n;
+       id += (int64_t)gridDim.x * blockDim.x)
+    slot[pos_n[id]] = pos_next[id];
+}
+
+// crd[pos[id]] = record of input element id
+__global__ void records_scatter_kernel(const uint32_t *pos, int64_t n, int nmodes,
+                                       const int32_t *coords, const float *vals, int32_t *crd,
+                                       float *val_out) {
+  const int cw = crd_words(nmodes);
+  const bool emb = value_embedded(nmodes);
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pos[id];
+    int32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < nmodes; ++q) w[q] = coords[id * nmodes + q];
+    const float v = vals[id];
+    if (emb) w[cw - 1] = __float_as_int(v);
+    else val_out[p] = v;
+    int4 *dst = reinterpret_cast<int4 *>(crd + p * cw);
+    dst[0] = make_int4(w[0], w[1], w[2], w[3]);
+    if (cw == 8) dst[1] = make_int4(w[4], w[5], w[6], w[7]);
+  }
 }
 
 __global__ void records_kernel(const uint32_t *order, int64_t n, int nmodes, const int32_t *coords,
@@ -244,7 +272,7 @@ int fc_value_embedded(int nmodes) { return (nmodes >= 2 && nmodes <= 8) ? (value
 int fc_build_morton(const int32_t *coords, int64_t nnz, int nmodes, const int64_t *m,
                     const int64_t *k, uint64_t *hi, uint64_t *lo, void *stream) {
   FC_CHECK_ARG(nmodes >= 2 && nmodes <= kMaxModes, "nmodes %d", nmodes);
-  FC_CHECK_ARG(coords && hi && lo && m && k, "null argument");
+  FC_CHECK_ARG(coords && lo && m && k, "null argument");
   MortonPlan mp{};
   mp.nmodes = nmodes;
   int total = 0;
@@ -259,6 +287,7 @@ int fc_build_morton(const int32_t *coords, int64_t nnz, int nmodes, const int64_
     set_error("morton key would need %d bits (> 128)", total);
     return FC_ERR_UNSUPPORTED;
   }
+  FC_CHECK_ARG(hi || total <= 64, "hi word needed for a %d-bit key", total);
   if (nnz == 0) return FC_OK;
   morton_kernel<<<grid_for(nnz), 256, 0, as_stream(stream)>>>(coords, nnz, mp, hi, lo);
   FC_LAUNCH_CHECK();
@@ -335,6 +364,25 @@ int fc_build_slots(const uint32_t *order, const uint32_t *pos_next, int64_t nnz,
                    void *stream) {
   if (nnz == 0) return FC_OK;
   slots_kernel<<<grid_for(nnz), 256, 0, as_stream(stream)>>>(order, pos_next, nnz, slot);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_build_slots_scatter(const uint32_t *pos_n, const uint32_t *pos_next, int64_t nnz,
+                           uint32_t *slot, void *stream) {
+  if (nnz == 0) return FC_OK;
+  slots_scatter_kernel<<<grid_for(nnz), 256, 0, as_stream(stream)>>>(pos_n, pos_next, nnz, slot);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_build_records_scatter(const uint32_t *pos, int64_t nnz, int nmodes, const int32_t *coords,
+                             const float *vals, void *crd, float *val_out, void *stream) {
+  FC_CHECK_ARG(nmodes >= 2 && nmodes <= kMaxModes, "nmodes %d", nmodes);
+  FC_CHECK_ARG(value_embedded(nmodes) || val_out, "separate value array required");
+  if (nnz == 0) return FC_OK;
+  records_scatter_kernel<<<grid_for(nnz), 256, 0, as_stream(stream)>>>(
+      pos, nnz, nmodes, coords, vals, static_cast<int32_t *>(crd), val_out);
   FC_LAUNCH_CHECK();
   return FC_OK;
 }

@@ -425,19 +425,29 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
     m_arr = _lib.i64_array(params.m)
     k_arr = _lib.i64_array(params.k)
 
+    # Memory-lean sequence (peak ~ coords + 2 sort key arrays + a few u32
+    # arrays; the billion-nonzero configs need it):
+    #   1. Morton keys, then ONE stable sort of element ids by (hi, lo):
+    #      the mode-independent "Morton order" (ties by input position);
+    #   2. per mode, canonical order = stable sort of the Morton order by
+    #      iv_n (= lexsort(seq, lo, hi, iv_n), layout.py:484); its histogram
+    #      gives the plan, and it is reduced to shard ids at once;
+    #   3. per mode, B200 order = stable sort of the Morton order by
+    #      (sid_n, sid_{n-1}); only its inverse (positions) is kept;
+    #   4. slot maps and the mode-0 records by scatter from positions.
     widths = [_bitlen(k - 1) for k in params.k]
     W = sum(widths)
-    hi = torch.empty(nnz, dtype=torch.int64, device=dev)
     lo = torch.empty(nnz, dtype=torch.int64, device=dev)
+    hi = torch.empty(nnz, dtype=torch.int64, device=dev) if W > 64 else None
     _lib.call("fc_build_morton", P(coords), nnz, N, m_arr, k_arr, P(hi), P(lo), st)
 
     temp_bytes = int(L.fc_build_sort_temp_bytes(max(nnz, 1)))
     temp = torch.empty(max(temp_bytes, 1), dtype=torch.uint8, device=dev)
     keys_a = torch.empty(nnz, dtype=torch.int64, device=dev)
     keys_b = torch.empty(nnz, dtype=torch.int64, device=dev)
-    iota = torch.arange(nnz, dtype=torch.int32, device=dev)
 
-    def sort_pass(ids, what, end_bit, mode=0, m=1, shift=0):
+    def sort_by(ids, what, end_bit, mode=0, m=1, shift=0):
+        """stable sort of `ids` by key f(id) on bits [0, end_bit)"""
         if end_bit <= 0:
             return ids
         _lib.call("fc_build_gather_key", P(ids), nnz, what, P(hi), P(lo), P(coords), N, mode, m,
@@ -447,48 +457,50 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
                   P(temp), temp_bytes, st)
         return out
 
-    orders, sids, counts_all = [], [], []
+    ids = torch.arange(nnz, dtype=torch.int32, device=dev)
+    morton = sort_by(ids, 0, min(W, 64))
+    if W > 64:
+        morton = sort_by(morton, 1, W - 64)
+    del ids, hi, lo
+    hi = lo = None
+
+    counts_all, sids = [], []
     hist = torch.empty(max(params.k), dtype=torch.int64, device=dev)
     for n in range(N):
-        B = _bitlen(params.k[n] - 1)
-        if W + B <= 64:
-            order = sort_pass(iota, 3, W + B, n, params.m[n], W)
-        else:
-            order = sort_pass(iota, 0, min(W, 64))
-            if W > 64:
-                order = sort_pass(order, 1, W - 64)
-            order = sort_pass(order, 2, B, n, params.m[n])
-        if order is iota:
-            order = iota.clone()
+        order = sort_by(morton, 2, _bitlen(params.k[n] - 1), n, params.m[n])
         _lib.call("fc_build_ss_hist", P(coords), nnz, N, n, params.m[n], params.k[n], P(hist), st)
-        counts_all.append(hist[: params.k[n]].cpu().numpy().astype(np.int64))
-        orders.append(order)
-    plan = plan_from_counts(params, counts_all)
-    if any(int(c.sum()) != nnz for c in counts_all):
-        raise ValueError("coordinates outside the declared dims")
-    for n in range(N):
-        offs = torch.from_numpy(plan.ss_elem_offsets[n]).to(dev)
-        first = torch.from_numpy(plan.ss_first_shard[n]).to(dev)
+        counts = hist[: params.k[n]].cpu().numpy().astype(np.int64)
+        if int(counts.sum()) != nnz:
+            raise ValueError("coordinates outside the declared dims")
+        counts_all.append(counts)
+        # this mode's super-shard offsets and first shard ids (layout.py:487-490)
+        offs = torch.from_numpy(np.concatenate(([0], np.cumsum(counts))).astype(np.int64)).to(dev)
+        first = torch.from_numpy(np.concatenate(([0], np.cumsum(-(-counts // params.g))))
+                                 .astype(np.int64)).to(dev)
         sid = torch.empty(nnz, dtype=torch.int32, device=dev)
-        _lib.call("fc_build_shard_ids", P(orders[n]), nnz, P(coords), N, n, params.m[n], P(offs),
+        _lib.call("fc_build_shard_ids", P(order), nnz, P(coords), N, n, params.m[n], P(offs),
                   P(first), params.g, P(sid), st)
         sids.append(sid)
-    gorders, gpos = [], []
+        del order
+    plan = plan_from_counts(params, counts_all)
+
+    gpos = []
     for n in range(N):
         prev = (n - 1) % N
         end_bit = 32 + _bitlen(plan.total_shards(n) - 1)
-        _lib.call("fc_build_device_key", P(orders[n]), nnz, P(sids[n]), P(sids[prev]), P(keys_a), st)
-        g_ord = torch.empty_like(orders[n])
-        _lib.call("fc_build_sort_pairs", P(keys_a), P(keys_b), P(orders[n]), P(g_ord), nnz,
+        _lib.call("fc_build_device_key", P(morton), nnz, P(sids[n]), P(sids[prev]), P(keys_a), st)
+        g_ord = torch.empty_like(morton)
+        _lib.call("fc_build_sort_pairs", P(keys_a), P(keys_b), P(morton), P(g_ord), nnz,
                   min(end_bit, 64), P(temp), temp_bytes, st)
         pos = torch.empty(nnz, dtype=torch.int32, device=dev)
         _lib.call("fc_build_invert", P(g_ord), nnz, P(pos), st)
-        gorders.append(g_ord)
         gpos.append(pos)
+        del g_ord
+    del sids, morton, keys_a, keys_b, temp
     slot_maps = []
     for n in range(N):
         slot = torch.empty(nnz, dtype=torch.int32, device=dev)
-        _lib.call("fc_build_slots", P(gorders[n]), P(gpos[(n + 1) % N]), nnz, P(slot), st)
+        _lib.call("fc_build_slots_scatter", P(gpos[n]), P(gpos[(n + 1) % N]), nnz, P(slot), st)
         slot_maps.append(slot)
     cw = int(L.fc_crd_words(N))
     emb = bool(L.fc_value_embedded(N))
@@ -496,7 +508,8 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
            torch.zeros((nnz, cw), dtype=torch.int32, device=dev)]
     val = [None, None] if emb else [torch.empty(nnz, dtype=torch.float32, device=dev),
                                     torch.zeros(nnz, dtype=torch.float32, device=dev)]
-    _lib.call("fc_build_records", P(gorders[0]), nnz, N, P(coords), P(fvals), P(crd[0]),
+    _lib.call("fc_build_records_scatter", P(gpos[0]), nnz, N, P(coords), P(fvals), P(crd[0]),
               P(val[0]), st)
+    del gpos
     torch.cuda.current_stream().synchronize()
     return DeviceShardedTensor(plan, crd, val, tuple(slot_maps), dev)

@@ -104,8 +104,7 @@ def zipf_tensor(dims: Sequence[int], nnz: int, seed: int, exponents: Sequence, d
     cdf_ptrs = _lib.ptr_array([c.data_ptr() if c is not None else 0 for c in cdfs])
     cdf_len = _lib.i64_array([c.numel() if c is not None else 0 for c in cdfs])
     dims_arr = _lib.i64_array(dims)
-    bits = sum(math.log2(d) for d in dims)
-    bits = int(math.ceil(bits)) + 1
+    bits = (math.prod(dims) - 1).bit_length()  # mixed-radix key width
     ndraws = int(nnz * draw_factor) + 1024
     while True:
         if ndraws >= 1 << 32:
@@ -117,39 +116,47 @@ def zipf_tensor(dims: Sequence[int], nnz: int, seed: int, exponents: Sequence, d
         lo = torch.empty(ndraws, dtype=torch.int64, device=dev)
         _lib.call("fc_synth_keys", coords.data_ptr(), ndraws, N, dims_arr, hi.data_ptr(),
                   lo.data_ptr(), strm)
+        if bits <= 64:
+            del hi
+            hi = None
         temp_bytes = int(L.fc_build_sort_temp_bytes(ndraws))
         temp = torch.empty(max(temp_bytes, 1), dtype=torch.uint8, device=dev)
         ids = torch.arange(ndraws, dtype=torch.int32, device=dev)
         ks = torch.empty_like(lo)
         ids2 = torch.empty_like(ids)
         _lib.call("fc_build_sort_pairs", lo.data_ptr(), ks.data_ptr(), ids.data_ptr(),
-                  ids2.data_ptr(), ndraws, min(bits, 64), temp.data_ptr(), temp_bytes, strm)
-        ids = ids2
+                  ids2.data_ptr(), ndraws, max(1, min(bits, 64)), temp.data_ptr(), temp_bytes, strm)
+        ids, ids2 = ids2, ids
         if bits > 64:
             kh = torch.empty_like(hi)
             _lib.call("fc_build_gather_key", ids.data_ptr(), ndraws, 1, hi.data_ptr(), lo.data_ptr(),
                       None, N, 0, 1, 0, kh.data_ptr(), strm)
-            ids3 = torch.empty_like(ids)
             _lib.call("fc_build_sort_pairs", kh.data_ptr(), ks.data_ptr(), ids.data_ptr(),
-                      ids3.data_ptr(), ndraws, bits - 64, temp.data_ptr(), temp_bytes, strm)
-            ids = ids3
-        hs = torch.empty_like(hi)
-        ls = torch.empty_like(lo)
-        _lib.call("fc_build_gather_key", ids.data_ptr(), ndraws, 1, hi.data_ptr(), lo.data_ptr(),
-                  None, N, 0, 1, 0, hs.data_ptr(), strm)
-        _lib.call("fc_build_gather_key", ids.data_ptr(), ndraws, 0, hi.data_ptr(), lo.data_ptr(),
-                  None, N, 0, 1, 0, ls.data_ptr(), strm)
+                      ids2.data_ptr(), ndraws, bits - 64, temp.data_ptr(), temp_bytes, strm)
+            ids = ids2
+            del kh
+            hs = torch.empty_like(hi)
+            _lib.call("fc_build_gather_key", ids.data_ptr(), ndraws, 1, hi.data_ptr(), lo.data_ptr(),
+                      None, N, 0, 1, 0, hs.data_ptr(), strm)
+            _lib.call("fc_build_gather_key", ids.data_ptr(), ndraws, 0, hi.data_ptr(), lo.data_ptr(),
+                      None, N, 0, 1, 0, ks.data_ptr(), strm)
+        else:
+            hs = ks  # the sorted low words are the whole key
+        del temp, lo
         keep = torch.zeros(ndraws, dtype=torch.uint8, device=dev)
-        _lib.call("fc_synth_mark_first", hs.data_ptr(), ls.data_ptr(), ids.data_ptr(), ndraws,
+        _lib.call("fc_synth_mark_first", hs.data_ptr(), ks.data_ptr(), ids.data_ptr(), ndraws,
                   keep.data_ptr(), strm)
-        del hs, ls, ks, hi, lo, temp, ids, ids2
+        del hs, ks, ids, ids2, hi
         kept = torch.nonzero(keep).squeeze(1)
+        del keep
         if kept.numel() >= nnz:
             sel = kept[:nnz]
+            del kept
             coords = coords.index_select(0, sel).contiguous()
             break
         # deterministic restart with more draws: draw j never depends on ndraws
         ratio = nnz / max(kept.numel(), 1)
+        del kept, coords
         ndraws = int(ndraws * max(1.2, min(4.0, ratio * 1.1))) + 1024
     vals = torch.empty(nnz, dtype=torch.float32, device=dev)
     _lib.call("fc_synth_uniform", int(seed), 77, nnz, vals.data_ptr(), 1, strm)

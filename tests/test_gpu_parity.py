@@ -335,3 +335,15 @@ def test_sparse_mode_direct_chunks():
             out = mttkrp_mode(st, DeviceFactorSet.from_host(fs), n, smap)
             assert_rel(out.double().cpu().numpy(), oracle.reference_mttkrp(subs, vals, fs, n),
                        what=f"direct R={rank} mode {n}")
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_gpu_generator_matches_host_twin(cfg):
+    """K6 (GPU Philox + bounded-Zipf + first-occurrence dedup) equals its
+    numpy twin: 64-bit keys (config 2 shape) and 128-bit keys (config 3)."""
+    from paper_2309_09131_b200.synth import CONFIGS, zipf_tensor_host
+    c = CONFIGS[cfg]
+    coords, vals = zipf_tensor(c["dims"], 200_000, seed=cfg, exponents=c["law"])
+    subs, hv = zipf_tensor_host(c["dims"], 200_000, seed=cfg, exponents=c["law"])
+    assert np.array_equal(coords.cpu().numpy().astype(np.int64), subs)
+    assert np.array_equal(vals.cpu().numpy(), hv)
