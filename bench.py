@@ -31,6 +31,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# the billion-nonzero configs build near the HBM limit: avoid fragmentation
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 METRIC = "all-mode spMTTKRP+remap sweep time & nnz/s at R=32; % HBM roofline; 1/2/4/8 GPU"
 UNIT = "nnz/s"

@@ -505,9 +505,9 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
     cw = int(L.fc_crd_words(N))
     emb = bool(L.fc_value_embedded(N))
     crd = [torch.empty((nnz, cw), dtype=torch.int32, device=dev),
-           torch.zeros((nnz, cw), dtype=torch.int32, device=dev)]
+           torch.empty((nnz, cw), dtype=torch.int32, device=dev)]
     val = [None, None] if emb else [torch.empty(nnz, dtype=torch.float32, device=dev),
-                                    torch.zeros(nnz, dtype=torch.float32, device=dev)]
+                                    torch.empty(nnz, dtype=torch.float32, device=dev)]
     _lib.call("fc_build_records_scatter", P(gpos[0]), nnz, N, P(coords), P(fvals), P(crd[0]),
               P(val[0]), st)
     del gpos
