@@ -14,6 +14,7 @@ from .layout import (DeviceShardedTensor, PartitionPlan, build_device_sharded, p
 from .params import (InfeasibleParamsError, PartitionParams, default_element_bytes,
                      device_params, element_size_bits, select_params)
 from .schedule import ScheduleMap, load_stats, schedule_super_shards
+from .cpals import CpalsConfig, CpalsResult, cp_als, fit, normalize_factors
 
 # reference-compatible aliases
 FactorSet = DeviceFactorSet

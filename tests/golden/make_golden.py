@@ -15,7 +15,8 @@ cases, everything the hot path is defined by:
 * ``sweep_all_modes`` results (engine.py:269-293);
 * ``reference_mttkrp`` outputs (coo.py:406-426);
 * a digest of ``synth_tensor`` for config 1 (coo.py:323-355), which the
-  package's uniform generator restates.
+  package's uniform generator restates;
+* ``cp_als`` fit histories, factors and ``fit`` (cpals.py:102-188).
 
 Usage:  NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py
 """
@@ -202,11 +203,40 @@ def golden_schedule():
     (OUT / "schedule.json").write_text(json.dumps(out))
 
 
+
+
+def golden_cpals():
+    """cp_als (cpals.py:123-188) on two small tensors; fp32-representable
+    values so the device run starts from the same numbers."""
+    out = {}
+    for name, dims, nnz, seed, rank, iters in (("a", (30, 40, 50), 3000, 21, 4, 8),
+                                               ("b", (9, 11, 7, 13), 800, 22, 3, 6)):
+        t = small_coo(seed, dims, nnz)
+        cfg = mc.CpalsConfig(rank=rank, max_iters=iters, tol=1e-12, seed=seed, nu=2,
+                             gamma=1 << 20, g_range=(16, 256))
+        res = mc.cp_als(t, cfg)
+        out[f"{name}_subs"] = t.subs
+        out[f"{name}_vals"] = t.vals
+        out[f"{name}_dims"] = np.asarray(dims)
+        out[f"{name}_cfg"] = np.asarray([rank, iters, seed])
+        out[f"{name}_fit"] = np.asarray(res.fit_history)
+        out[f"{name}_lambdas"] = res.factors.lambdas
+        for n, f in enumerate(res.factors.factors):
+            out[f"{name}_factor{n}"] = f
+        out[f"{name}_fit_fn"] = np.asarray([mc.fit(t, res.factors)])
+    np.savez_compressed(OUT / "cpals.npz", **out)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nc")
+    only = os.environ.get("GOLDEN_ONLY")  # e.g. GOLDEN_ONLY=cpals regenerates one fixture
+    if only:
+        globals()[f"golden_{only}"]()
+        sys.exit(0)
     golden_params()
     golden_morton()
     golden_layouts()
     golden_synth()
     golden_schedule()
+    golden_cpals()
     print("golden fixtures written to", OUT)
