@@ -227,6 +227,19 @@ def golden_cpals():
     np.savez_compressed(OUT / "cpals.npz", **out)
 
 
+def golden_io():
+    """MCFD factor dump bytes (coo.py:433-447) and FROSTT parse/write
+    (coo.py:212-316)."""
+    fs = mc.FactorSet.random((5, 7, 3), 4, seed=2)
+    fs = mc.FactorSet(fs.factors, np.array([1.0, 2.0, 0.5, 3.0]))
+    (OUT / "mcfd_small.bin").write_bytes(mc.save_factor_set(fs, None))
+    t = mc.synth_tensor((6, 5, 4), 40, seed=3, skew=0.4)
+    (OUT / "frostt_small.tns").write_text(mc.write_frostt(t))
+    t2 = mc.parse_frostt("# comment\n1 1 1 1.5\n2 3 1 2.0\n1 1 1 0.25\n\n3 2 2 -1\n")
+    np.savez_compressed(OUT / "frostt_parse.npz", subs=t2.subs, vals=t2.vals,
+                        dims=np.asarray(t2.dims), synth_subs=t.subs, synth_vals=t.vals)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nc")
     only = os.environ.get("GOLDEN_ONLY")  # e.g. GOLDEN_ONLY=cpals regenerates one fixture
@@ -239,4 +252,5 @@ if __name__ == "__main__":
     golden_synth()
     golden_schedule()
     golden_cpals()
+    golden_io()
     print("golden fixtures written to", OUT)

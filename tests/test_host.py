@@ -142,3 +142,44 @@ def test_mode_work_merges_small_super_shards():
         assert np.all(owner == 1), n
     w0 = make_mode_work(plan, 0, 32, "cpu", chunk_elems=4096)
     assert (w0.chunk_part.numpy() == PART_DIRECT).any() and w0.hist_rows > params.m[0]
+
+
+def test_mcfd_dump_byte_compatible_with_reference():
+    """Our MCFD writer reproduces the reference's bytes; the reader round-trips."""
+    import struct as _s
+    from paper_2309_09131_b200 import io as fio
+    blob = (GOLDEN / "mcfd_small.bin").read_bytes()
+    _, _, nm = _s.unpack_from("<4sII", blob, 0)
+    rows = _s.unpack_from(f"<{nm}Q", blob, 12)
+    rank = _s.unpack_from("<I", blob, 12 + 8 * nm)[0]
+    off = 12 + 8 * nm + 5
+    lam = np.frombuffer(blob, "<f8", rank, off)
+    off += 8 * rank
+    mats = []
+    for r in rows:
+        mats.append(np.frombuffer(blob, "<f8", r * rank, off).reshape(r, rank))
+        off += 8 * r * rank
+
+    class FS:
+        factors = mats
+        lambdas = lam
+    assert fio.save_factor_set(FS()) == blob
+    with pytest.raises(ValueError, match="magic"):
+        fio.load_factor_set(b"XXXX" + b"\0" * 32, device="cpu")
+
+
+def test_frostt_parse_and_write_match_reference():
+    from paper_2309_09131_b200 import io as fio
+    z = np.load(GOLDEN / "frostt_parse.npz")
+    subs, vals, dims = fio.parse_frostt("# comment\n1 1 1 1.5\n2 3 1 2.0\n1 1 1 0.25\n\n3 2 2 -1\n")
+    assert np.array_equal(subs, z["subs"]) and np.array_equal(vals, z["vals"])
+    assert tuple(dims) == tuple(z["dims"])
+    ref_text = (GOLDEN / "frostt_small.tns").read_text()
+    assert fio.write_frostt(z["synth_subs"], z["synth_vals"]) == ref_text
+    s2, v2, _ = fio.parse_frostt(ref_text)
+    o = np.lexsort(z["synth_subs"].T[::-1])
+    assert np.array_equal(s2, z["synth_subs"][o]) and np.array_equal(v2, z["synth_vals"][o])
+    for bad, line in (("1 1 1.5 2\n", 1), ("1 1 1\n0 1 2\n", 2), ("1 2 3\n1 2\n", 2)):
+        with pytest.raises(fio.FrosttParseError) as e:
+            fio.parse_frostt(bad)
+        assert e.value.lineno == line
