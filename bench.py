@@ -41,8 +41,8 @@ UNIT = "nnz/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (same law)")
@@ -379,7 +379,10 @@ def run_reference(args, rank, world, local):
     if rank != 0:
         return
     cfg = workload(args.config, args.nnz)
-    sample = args.cpu_sample or min(cfg["nnz"], 8_000_000)
+    # bounded sample: 8M nonzeros (~0.5 s per sweep on a 16-core host) up to
+    # ~150 sweeps, shrinking beyond that so the reference arm stays ~1-2 min
+    budget = int(8_000_000 * 150 / max(args.steps + args.warmup, 150))
+    sample = args.cpu_sample or min(cfg["nnz"], max(200_000, budget))
     res = cpu_baseline(args.config, cfg, sample, steps=max(args.steps, 1), warmup=max(args.warmup, 0))
     N = len(cfg["dims"])
     line = {
