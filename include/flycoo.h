@@ -89,10 +89,13 @@ int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);
  *   zero on entry.
  * Slots must be < nnz, the destination capacity (on one GPU the buffer
  * size; multi-GPU: local part + send region, see dist.py).
+ * `dims` (optional) lets 3-mode tensors whose two input coordinates fit 32
+ * bits use 8-byte sorted records (same results, less shared traffic).
  * counters[0] += elements processed (the engine.py:335-338 check).        */
 int fc_mode_worker(const void *src_crd, const float *src_val,
                    void *dst_crd, float *dst_val,
                    const float *const *factors, /* host array, N device ptrs */
+                   const int64_t *dims,         /* host array, N (may be NULL) */
                    float *out, int nmodes, int mode, int rank,
                    int64_t out_rows, int64_t m_mode,
                    const int64_t *chunk_start, const int32_t *chunk_ss,

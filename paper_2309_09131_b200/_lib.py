@@ -34,7 +34,7 @@ _SIGS = {
     "fc_chunk_rows_max": (_i64, [_int, _int, _i64]),
     "fc_mode_worker": (_int, [
         _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val
-        _vp, _vp,                      # factors (host array of device ptrs), out
+        _vp, _vp, _vp,                 # factors (host array of device ptrs), dims (host), out
         _int, _int, _int,              # nmodes, mode, rank
         _i64, _i64,                    # out_rows, m_mode
         _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks

@@ -10,6 +10,7 @@
 
 #include "pipe_kernel.cuh"
 #include "warp_kernel.cuh"
+#include "pack_kernel.cuh"
 
 namespace fc {
 
@@ -25,8 +26,22 @@ inline int kernel_kind() {
   return v;
 }
 
+inline bool pack_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("FLYCOO_PACK");
+    v = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NM, int MODE, int LPG, int RT>
 int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  if constexpr (NM == 3) {
+    // 8-byte sorted records when the two input coordinates fit 32 bits
+    if (a.pack_shift > 0 && kernel_kind() == 1 && pack_enabled())
+      return launch_pack<MODE, LPG, RT>(a, nchunks, st);
+  }
   // direct chunks (hist_rows > tile_rows) exist only in the tile kernel
   if (a.hist_rows > a.tile_rows) return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
   switch (kernel_kind()) {

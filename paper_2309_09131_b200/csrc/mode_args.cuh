@@ -25,6 +25,8 @@ struct ModeArgs {
   const int32_t *chunk_rows;  // rows of a chunk merging several small super-shards (or null)
   int64_t tile_rows;          // accumulator tile height (>= m): max rows of non-direct chunks
   int64_t hist_rows;          // max rows of any chunk (counting-sort bins, <= 256)
+  int pack_shift;             // N = 3: width of the second input coordinate when both
+                              // input coordinates fit 32 bits (8-B sorted records), else 0
   float *part_ws;
   const uint32_t *slots;
   int64_t nnz;

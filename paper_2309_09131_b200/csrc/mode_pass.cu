@@ -485,7 +485,8 @@ int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m) {
 }
 
 int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
-                   const float *const *factors, float *out, int nmodes, int mode, int rank,
+                   const float *const *factors, const int64_t *dims, float *out, int nmodes,
+                   int mode, int rank,
                    int64_t out_rows, int64_t m_mode, const int64_t *chunk_start,
                    const int32_t *chunk_ss, const int32_t *chunk_part,
                    const int32_t *chunk_rows, int64_t tile_rows, int64_t hist_rows,
@@ -554,6 +555,15 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
   a.chunk_rows = chunk_rows;
   a.tile_rows = chunk_rows ? tile_rows : m_mode;
   a.hist_rows = chunk_rows ? (hist_rows > a.tile_rows ? hist_rows : a.tile_rows) : m_mode;
+  a.pack_shift = 0;
+  if (dims && nmodes == 3) {
+    for (int w = 0; w < nmodes; ++w)
+      FC_CHECK_ARG(dims[w] >= 1 && dims[w] <= INT32_MAX, "dims[%d] out of range", w);
+    const int w1 = mode == 0 ? 1 : 0, w2 = mode == 2 ? 1 : 2;
+    const int b1 = bit_length_u64((uint64_t)(dims[w1] - 1));
+    const int b2 = bit_length_u64((uint64_t)(dims[w2] - 1));
+    if (b2 >= 1 && b1 + b2 <= 32) a.pack_shift = b2;
+  }
   a.part_ws = part_ws;
   a.slots = dest_slots;
   a.nnz = nnz;

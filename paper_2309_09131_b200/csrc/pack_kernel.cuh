@@ -1,0 +1,355 @@
+// K1, packed-record variant of the tile kernel for 3-mode tensors whose two
+// non-output coordinates fit 32 bits together (config 2: 14 + 15 bits).
+//
+// Same phases and the same sums as mode_pass_fast_kernel (fast_kernel.cuh),
+// but the sorted tile holds 8-byte records {c_w1 << shift | c_w2, value}
+// instead of 16-byte ones, and phase C takes row boundaries from the sort's
+// bin offsets instead of reading a row per element:
+//   * shared traffic of the sorted tile halves (one 64-bit load serves the
+//     group; the scatter of 8-B records conflicts less);
+//   * the tile shrinks by 16 KB, which the SM gives back to L1 -- where the
+//     factor-row gathers hit.
+#pragma once
+
+#include "fast_kernel.cuh"
+
+namespace fc {
+
+template <int LPG>
+struct PackPlan {
+  static constexpr int G = kFBlock / LPG;
+  static constexpr int P = kFTile / G;
+  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + G);
+  static constexpr size_t misc_bytes = 4 * (kFWarps + 4 + G);
+  static constexpr size_t fixed_bytes = sorted_bytes + misc_bytes;
+  __host__ __device__ static size_t hist_bytes(int64_t m) {
+    return sizeof(int) * kFWarps * ((m + 3) / 4 * 4);
+  }
+  static size_t total(int rank, int64_t m, int64_t hist_rows) {
+    return fixed_bytes + hist_bytes(hist_rows > m ? hist_rows : m) + (size_t)2 * G * sizeof(int) +
+           (size_t)2 * G * rank * sizeof(float) + (size_t)m * rank * sizeof(float);
+  }
+};
+
+template <int MODE, int LPG, int RT>
+__global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_pack_kernel(const ModeArgs a) {
+  using PP = PackPlan<LPG>;
+  constexpr int G = PP::G;
+  constexpr int P = PP::P;
+  constexpr int U = FAST_U;
+  constexpr int W1 = MODE == 0 ? 1 : 0;  // the two input modes, ascending
+  constexpr int W2 = MODE == 2 ? 1 : 2;
+  const int R = RT > 0 ? RT : a.rank;
+  const int shift = a.pack_shift;
+  const uint32_t lowmask = (1u << shift) - 1u;
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
+  uint2 *s_sorted = reinterpret_cast<uint2 *>(smem);
+  int *s_misc = reinterpret_cast<int *>(smem + PP::sorted_bytes);
+  int *s_piece_bin = s_misc + kFWarps + 4;  // first bin of every piece
+  unsigned char *tail = smem + PP::fixed_bytes;
+  int *s_hist = reinterpret_cast<int *>(tail);
+  tail += PP::hist_bytes(a.hist_rows);
+  int *s_bnd_row = reinterpret_cast<int *>(tail);
+  tail += 2 * G * sizeof(int);
+  float *s_bnd = reinterpret_cast<float *>(tail);
+  tail += (size_t)2 * G * R * sizeof(float);
+  float *s_acc = reinterpret_cast<float *>(tail);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t chunk = blockIdx.x;
+  const int64_t start = a.chunk_start[chunk];
+  const int64_t end = a.chunk_start[chunk + 1];
+  const int part = a.chunk_part[chunk];
+  const int64_t row0 = a.chunk_ss[chunk] * a.m;
+  const int rows = chunk_row_count(a, chunk, row0);
+  const int irow0 = (int)row0;
+  const bool direct = part == kPartDirect;
+  float *out_rows = a.out + row0 * R;
+  if (direct) {
+    if (start == end) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = tid; i < rows * R / 4; i += kFBlock) reinterpret_cast<float4 *>(out_rows)[i] = z;
+      return;
+    }
+  } else {
+    for (int i = tid; i < rows * R; i += kFBlock) s_acc[i] = 0.f;
+  }
+
+  const int gi = tid / LPG;
+  const int lg = tid % LPG;
+  const int col = lg * 4;
+  const bool col_ok = RT > 0 ? true : col < R;
+  auto phys = [](int pos) { return pos + pos / P; };
+  auto key_of = [&](const int4 &r) {
+    const int lr = comp<MODE>(r) - irow0;
+    return (lr >= 0 && lr < rows) ? lr : -1;
+  };
+  // start of bin k in the sorted tile (warp 0's base), end = start of k + 1
+  auto bin_start = [&](int k) { return s_hist[k]; };
+
+  for (int64_t t0 = start; t0 < end; t0 += kFTile) {
+    const int cnt = (int)min64(kFTile, end - t0);
+    // ---------------------------------------------------------------- A
+    int4 rec[kFIPT];
+    uint32_t slot[kFIPT];
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+      const int e = j * kFBlock + tid;
+      if (e < cnt) {
+        const int64_t i = t0 + e;
+        rec[j] = ld_stream_v4(a.src + i);
+        if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
+      } else {
+        rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
+      }
+    }
+    for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+      const int e = j * kFBlock + tid;
+      if (e < cnt) {
+        if (a.do_remap) {
+          const uint64_t s = slot[j];
+          if (s < (uint64_t)a.nnz) a.dst[s] = rec[j];
+          else atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
+        }
+        if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
+      }
+    }
+    __syncwarp();
+    // ---------------------------------------------------------------- B
+    int *wh = s_hist + warp * hstride;
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+      const int k = key_of(rec[j]);
+      const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
+      int old = 0;
+      if (k >= 0) old = wh[k];
+      __syncwarp();
+      if (k >= 0 && lane == __ffs(grp) - 1) wh[k] = old + __popc(grp);
+      __syncwarp();
+      set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
+    }
+    __syncthreads();
+    {
+      int tot = 0;
+      if (tid < rows) {
+#pragma unroll 4
+        for (int w = 0; w < kFWarps; ++w) tot += s_hist[w * hstride + tid];
+        if (direct && tot == 0) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
+        }
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_misc[warp] = incl;
+      __syncthreads();
+      int wpre = 0;
+#pragma unroll 4
+      for (int w = 0; w < kFWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
+      if (tid == kFBlock - 1) s_misc[kFWarps] = wpre + incl;
+      if (tid < rows) {
+        const int bstart = wpre + incl - tot;
+        int base = bstart;
+#pragma unroll 4
+        for (int w = 0; w < kFWarps; ++w) {
+          const int c = s_hist[w * hstride + tid];
+          s_hist[w * hstride + tid] = base;
+          base += c;
+        }
+        // pieces whose first element falls in this (non-empty) bin
+        for (int j = (bstart + P - 1) / P; j * P < bstart + tot; ++j) s_piece_bin[j] = tid;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kFIPT; ++j) {
+      const int x = comp<MODE>(rec[j]);
+      if (x >= 0) {
+        const int k = x & 255;
+        const int pos = wh[k] + (x >> 8);
+        const uint32_t pk = ((uint32_t)comp<W1>(rec[j]) << shift) | (uint32_t)comp<W2>(rec[j]);
+        s_sorted[phys(pos)] = make_uint2(pk, (uint32_t)rec[j].w);
+      }
+    }
+    __syncthreads();
+    const int nvalid = s_misc[kFWarps];
+    // ---------------------------------------------------------------- C
+    if (tid == 0 && t0 + kFTile < end) {
+      const int64_t n1 = min64(kFTile, end - (t0 + kFTile));
+      prefetch_l2(a.src + (t0 + kFTile), n1 * sizeof(int4));
+      if (a.do_remap) prefetch_l2(a.slots + (t0 + kFTile), n1 * sizeof(uint32_t));
+    }
+    if (lg == 0) {
+      s_bnd_row[2 * gi] = -1;
+      s_bnd_row[2 * gi + 1] = -1;
+    }
+    if (col_ok) {
+      const float z[4] = {0.f, 0.f, 0.f, 0.f};
+      VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
+      VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
+    }
+    const int pb = gi * P;
+    const int pe = min(pb + P, nvalid);
+    if (pb < pe) {
+      int cur = s_piece_bin[gi];
+      int nxt = cur + 1 < rows ? bin_start(cur + 1) : nvalid;
+      bool head = pb > bin_start(cur);
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      auto flush = [&]() {
+        if (head) {
+          if (lg == 0) s_bnd_row[2 * gi] = cur;
+          if (col_ok) VecT<4>::store(s_bnd + (2 * gi) * R + col, acc);
+        } else if (col_ok) {
+          if (direct) {
+            VecT<4>::store(out_rows + cur * R + col, acc);
+            return;
+          }
+          float *p = s_acc + cur * R + col;
+          float o[4];
+          VecT<4>::load(p, o);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) o[v] += acc[v];
+          VecT<4>::store(p, o);
+        }
+      };
+      auto consume = [&](int p, float v, const float (&pr)[4]) {
+        if (p == nxt) {  // a new row starts here
+          flush();
+          head = false;
+          do {
+            ++cur;
+            nxt = cur + 1 < rows ? bin_start(cur + 1) : nvalid;
+          } while (nxt == p);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = fmaf(v, pr[k], acc[k]);
+      };
+      auto prod = [&](uint32_t pk, float (&pr)[4]) {
+        const uint32_t c1 = pk >> shift, c2 = pk & lowmask;
+        const float4 f1 = __ldg(reinterpret_cast<const float4 *>(
+            a.fac[W1] + (uint64_t)c1 * (uint32_t)(RT > 0 ? RT : R) + col));
+        const float4 f2 = __ldg(reinterpret_cast<const float4 *>(
+            a.fac[W2] + (uint64_t)c2 * (uint32_t)(RT > 0 ? RT : R) + col));
+        pr[0] = f1.x * f2.x;
+        pr[1] = f1.y * f2.y;
+        pr[2] = f1.z * f2.z;
+        pr[3] = f1.w * f2.w;
+      };
+      const uint2 *sp = s_sorted + gi;  // pad of piece gi
+      int p = pb;
+      for (; p + U <= pe; p += U) {
+        uint2 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) q[u] = sp[p + u];
+        float pr[U][4];
+        if (col_ok) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) prod(q[u].x, pr[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) consume(p + u, __uint_as_float(q[u].y), pr[u]);
+      }
+      for (; p < pe; ++p) {
+        const uint2 q = sp[p];
+        float pr[4];
+        if (col_ok) prod(q.x, pr);
+        consume(p, __uint_as_float(q.y), pr);
+      }
+      const bool tail = pe < nvalid && nxt > pe;
+      if (tail && !head) {
+        if (lg == 0) s_bnd_row[2 * gi + 1] = cur;
+        if (col_ok) VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, acc);
+      } else {
+        flush();
+      }
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- D
+    {
+      constexpr int E = (2 * G + kFWarps - 1) / kFWarps;
+      constexpr int RC = (LPG * 4 + 31) / 32;
+      const int ent0 = warp * E;
+      const int ent_end = min(2 * G, ent0 + E);
+      int prev = -1;
+      for (int e2 = ent0 - 1; e2 >= 0; --e2) {
+        const int r2 = s_bnd_row[e2];
+        if (r2 >= 0) {
+          prev = r2;
+          break;
+        }
+      }
+      for (int ent = ent0; ent < ent_end; ++ent) {
+        const int row = s_bnd_row[ent];
+        if (row < 0 || row == prev) {
+          if (row >= 0) prev = row;
+          continue;
+        }
+        prev = row;
+        int e3 = ent + 1;
+        while (e3 < 2 * G) {
+          const int r3 = s_bnd_row[e3];
+          if (r3 >= 0 && r3 != row) break;
+          ++e3;
+        }
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+          const int c = q * 32 + lane;
+          if (c < R) {
+            float run = 0.f;
+            int e = ent;
+            for (; e + 4 <= e3; e += 4) {
+              const float x0 = s_bnd[e * R + c], x1 = s_bnd[(e + 1) * R + c];
+              const float x2 = s_bnd[(e + 2) * R + c], x3 = s_bnd[(e + 3) * R + c];
+              run += x0;
+              run += x1;
+              run += x2;
+              run += x3;
+            }
+            for (; e < e3; ++e) run += s_bnd[e * R + c];
+            if (direct) out_rows[row * R + c] = run;
+            else s_acc[row * R + c] += run;
+          }
+        }
+      }
+    }
+  }
+  if (!direct) {
+    __syncthreads();
+    float *dstp = part < 0 ? out_rows : a.part_ws + (int64_t)part * a.m * R;
+    const int n4 = rows * R / 4;
+    const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
+    float4 *d4 = reinterpret_cast<float4 *>(dstp);
+    for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
+  }
+  if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
+}
+
+template <int MODE, int LPG, int RT>
+int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
+  const size_t smem = PackPlan<LPG>::total(a.rank, a.tile_rows, a.hist_rows);
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  if (nchunks > 0) {
+    kern<<<(unsigned)nchunks, kFBlock, smem, st>>>(a);
+    FC_LAUNCH_CHECK();
+  }
+  return FC_OK;
+}
+
+}  // namespace fc

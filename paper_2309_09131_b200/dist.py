@@ -222,7 +222,7 @@ class CudaOps:
         vp = lambda t: t.data_ptr() if t is not None else None
         params = dt.plan.params
         _lib.call("fc_mode_worker", dt.crd[a].data_ptr(), vp(dt.val[a]), dt.crd[b].data_ptr(),
-                  vp(dt.val[b]), fptrs, out.data_ptr(), dt.num_modes, mode, R, params.dims[mode],
+                  vp(dt.val[b]), fptrs, _lib.i64_array(params.dims), out.data_ptr(), dt.num_modes, mode, R, params.dims[mode],
                   params.m[mode], w.chunk_start.data_ptr(), w.chunk_ss.data_ptr(),
                   w.chunk_part.data_ptr(),
                   w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(), w.nred1, w.red2.data_ptr(),

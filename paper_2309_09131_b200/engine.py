@@ -230,7 +230,7 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
     val_p = lambda t: t.data_ptr() if t is not None else None
     for do_compute, do_remap in passes:
         _lib.call("fc_mode_worker", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
-                  val_p(st.val[b]), fptrs, out.data_ptr(), nmodes, mode, rank, dims[mode],
+                  val_p(st.val[b]), fptrs, _lib.i64_array(params.dims), out.data_ptr(), nmodes, mode, rank, dims[mode],
                   params.m[mode], work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),
                   work.chunk_part.data_ptr(),
                   work.chunk_rows.data_ptr() if work.chunk_rows is not None else None,

@@ -31,7 +31,7 @@ def timed(layout, mode, comp, remap, reps=5):
     vp = lambda t: t.data_ptr() if t is not None else None
 
     def once():
-        _lib.call("fc_mode_worker", crd.data_ptr(), None, dst.data_ptr(), None, fptrs,
+        _lib.call("fc_mode_worker", crd.data_ptr(), None, dst.data_ptr(), None, fptrs, _lib.i64_array(dims),
                   out.data_ptr(), N, mode, R, dims[mode], params.m[mode], w.chunk_start.data_ptr(),
                   w.chunk_ss.data_ptr(), w.chunk_part.data_ptr(),
                   w.chunk_rows.data_ptr() if w.chunk_rows is not None else None, w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(),
