@@ -64,6 +64,11 @@ __device__ __forceinline__ float ld_stream_f32(const float *p) {
   return r;
 }
 
+// Prefetch the line holding p into L1 (no register destination).
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Bulk prefetch of [p, p + bytes) into L2 (TMA unit).  The instruction
 // needs a 16-B aligned address and a multiple of 16 bytes: widen the range.
 __device__ __forceinline__ void prefetch_l2(const void *p, int64_t bytes) {
