@@ -137,6 +137,17 @@ def describe(cfg_index: int, cfg: dict) -> str:
             f"{cfg['semantics']}-factor sweep, fp32 values/factors U(0,1)")
 
 
+def kernel_name(N: int, dims, rank: int) -> str:
+    """The K1 instance the library dispatches for this shape (dispatch.cuh)."""
+    if os.environ.get("FLYCOO_KERNEL") in ("warp", "pipe"):
+        return f"mode_pass_{os.environ['FLYCOO_KERNEL']}_kernel"
+    if N == 3 and rank % 4 == 0 and rank <= 64 and os.environ.get("FLYCOO_PACK") != "0":
+        w = [(d - 1).bit_length() for d in dims]
+        if all(sum(w) - w[n] <= 32 for n in range(3)):
+            return "mode_pass_pack_kernel (8-B sorted records)"
+    return "mode_pass_fast_kernel"
+
+
 def compulsory_bytes(nnz: int, dims, rank: int):
     """Per mode-pass algorithmic bytes: records read + written,
     one uint32 slot read per element, each factor read once, output written
@@ -361,7 +372,7 @@ def run_ours(args, rank, world, local):
                        "mode_ms": [round(1e3 * x, 4) for x in mode_secs[:N]]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "mode_pass_fast_kernel (+ reduce_level_kernel)",
+                         "kernel": kernel_name(N, dims, R) + " (+ reduce_level_kernel)",
                          "algorithmic_bytes_per_launch": per_mode[0], "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches_per_step * args.steps,
