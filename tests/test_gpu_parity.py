@@ -347,3 +347,44 @@ def test_gpu_generator_matches_host_twin(cfg):
     subs, hv = zipf_tensor_host(c["dims"], 200_000, seed=cfg, exponents=c["law"])
     assert np.array_equal(coords.cpu().numpy().astype(np.int64), subs)
     assert np.array_equal(vals.cpu().numpy(), hv)
+
+
+def test_packed_and_unpacked_modes_in_one_sweep():
+    """Modes 0/1 fit 8-byte packed records (17 + 7 coordinate bits), mode 2
+    does not (17 + 17 > 32) and runs the 16-byte tile kernel; the chained
+    sweep must match the oracle through both."""
+    dims = (1 << 17, 1 << 17, 100)
+    coords, vals = zipf_tensor(dims, 400_000, seed=12, exponents=(0.8, 0.8, 1.0))
+    subs = coords.cpu().numpy().astype(np.int64)
+    v64 = vals.cpu().numpy().astype(np.float64)
+    assert subs[:, 0].max() >= 1 << 16 and subs[:, 1].max() >= 1 << 16
+    params = device_params(dims, len(v64), 32)
+    st = build_device_sharded(coords, vals, params)
+    smap = schedule_super_shards(st.plan, 1)
+    f0 = factors_f32(dims, 32, 9)
+    res = sweep_all_modes(st, DeviceFactorSet.from_host(f0), smap).to_numpy()
+    working = [f.astype(np.float64) for f in f0]
+    for n in range(3):
+        want = oracle.reference_mttkrp(subs, v64, working, n)
+        assert_rel(res[n], want, what=f"mixed mode {n}")
+        working[n] = res[n]
+
+
+def test_remap_store_single_element_mirror():
+    """remap_store / RemapCursors (engine.py:182-223): first store lands at the
+    shard base, a full shard raises ShardOverflowError."""
+    from paper_2309_09131_b200 import RemapCursors, remap_store
+    z, N, params = _golden("n3_small")
+    st = build_device_sharded(z["subs"], z["vals"], params)
+    cur = RemapCursors.for_mode(st, 1)
+    sids = st.shard_ids()
+    shard = int(sids[0, 1])
+    slot = remap_store(0, 1, cur, st)
+    assert slot == int(st.plan.shard_offsets[1][shard])
+    rec = st.crd[1 - st.active][slot].cpu()
+    assert torch.equal(rec, st.crd[st.active][0].cpu())
+    fill = cur.planned_fill(shard)
+    cur.fills[shard] = fill
+    with pytest.raises(ShardOverflowError):
+        remap_store(0, 1, cur, st)
+    assert not cur.complete()
