@@ -13,6 +13,15 @@
 
 #include "fast_kernel.cuh"
 
+// 4 CTAs/SM (its shared footprint is ~36 KB), 2 elements in flight per
+// group: no spills at the 64-register cap (profiles/r1_kernel_experiments.md)
+#ifndef PACK_MIN_BLOCKS
+#define PACK_MIN_BLOCKS 4
+#endif
+#ifndef PACK_U
+#define PACK_U 2
+#endif
+
 namespace fc {
 
 template <int LPG>
@@ -32,11 +41,11 @@ struct PackPlan {
 };
 
 template <int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_pack_kernel(const ModeArgs a) {
+__global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const ModeArgs a) {
   using PP = PackPlan<LPG>;
   constexpr int G = PP::G;
   constexpr int P = PP::P;
-  constexpr int U = FAST_U;
+  constexpr int U = PACK_U;
   constexpr int W1 = MODE == 0 ? 1 : 0;  // the two input modes, ascending
   constexpr int W2 = MODE == 2 ? 1 : 2;
   const int R = RT > 0 ? RT : a.rank;
