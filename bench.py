@@ -216,11 +216,24 @@ def run_ours(args, rank, world, local):
                                        schedule_super_shards, sweep_all_modes)
     from paper_2309_09131_b200.synth import config_tensor
 
+    # FLYCOO_PG_BACKEND=gloo: host-side process group for the p2p exchange
+    # (it needs only barriers and handle exchange), which also lets several
+    # ranks share one GPU for a functional smoke run -- never a measurement
+    backend = os.environ.get("FLYCOO_PG_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x: float) -> float:
+        tt = torch.tensor([x], device="cpu" if backend == "gloo" else dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
     cfg = workload(args.config, args.nnz)
     N, R, nnz, dims = len(cfg["dims"]), cfg["rank"], cfg["nnz"], cfg["dims"]
 
@@ -236,14 +249,24 @@ def run_ours(args, rank, world, local):
     smap = schedule_super_shards(st.plan, 1)
     factors = DeviceFactorSet.random(dims, R, seed=1000 + args.config, device=dev)
     updated = cfg["semantics"] == "updated"
+    exchange = os.environ.get("FLYCOO_EXCHANGE", "p2p")
     dt = None
     if world > 1:
         # partitioned sweep: every rank builds the same global layout, keeps
         # its slices + static exchange plan, and frees the rest
+        # exchange: "p2p" (default) = remap fused with the exchange, records
+        # stored into the owners' buffers over NVLink (peer.py); "nccl" =
+        # send region + all_to_all_single + unpack (dist.py)
         from paper_2309_09131_b200.dist import (CudaOps, DistShardedTensor, dist_mttkrp_mode,
                                                 dist_sweep_all_modes)
+        from paper_2309_09131_b200.peer import (PeerShardedTensor, peer_mttkrp_mode,
+                                                peer_sweep_all_modes)
         t0 = time.perf_counter()
-        dt = DistShardedTensor(st, world, rank)
+        if exchange == "p2p":
+            dt = PeerShardedTensor(st, world, rank)
+            dt.connect()
+        else:
+            dt = DistShardedTensor(st, world, rank)
         plan_s = time.perf_counter() - t0
         del st
         torch.cuda.empty_cache()
@@ -251,6 +274,12 @@ def run_ours(args, rank, world, local):
 
     def step(fs, mode_secs=None):
         flist = fs.factors if hasattr(fs, "factors") else fs
+        if dt is not None and exchange == "p2p":
+            if updated:
+                return peer_sweep_all_modes(dt, list(flist), mode_seconds=mode_secs)
+            outs = [peer_mttkrp_mode(dt, list(flist), n).clone() for n in range(N)]
+            dt.check()
+            return outs
         if dt is not None:
             if updated:
                 return dist_sweep_all_modes(dt, list(flist), ops, mode_seconds=mode_secs)
@@ -292,9 +321,7 @@ def run_ours(args, rank, world, local):
     t_ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if world > 1:
-        tt = torch.tensor([t_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+        t_ms = max_over_ranks(t_ms)
     ms_per_step = t_ms / args.steps
     # strong scaling for world > 1: the ranks share one tensor
     value = N * nnz / (ms_per_step / 1e3)
@@ -307,8 +334,8 @@ def run_ours(args, rank, world, local):
     achieved = sum(per_mode) / world * args.steps / kern_s / 1e9
     peak, peak_src = peaks()
     src = dt if dt is not None else st
-    launches_per_step = sum(src.mode_work(n, R).launches + (1 if dt is not None else 0)
-                            for n in range(N))
+    launches_per_step = sum(src.mode_work(n, R).launches +
+                            (1 if dt is not None and exchange != "p2p" else 0) for n in range(N))
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
@@ -342,9 +369,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.steps
         if world > 1:
-            tt = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e_ms = float(tt.item())
+            e_ms = max_over_ranks(e_ms)
         e2e = {"value": N * nnz / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
                "path": "sweep_all_modes(DeviceShardedTensor, factors<-pinned host) -> pinned host"}
@@ -365,8 +390,12 @@ def run_ours(args, rank, world, local):
                        "params_g": params.g, "l2": "inputs larger than L2 (records "
                        f"{nnz * (4 * N + 4) / 1e9:.2f} GB + slots {nnz * 4 * N / 1e9:.2f} GB vs 126 MB L2)",
                        "parallelism": "1 GPU" if world == 1 else
-                       f"dp{world}: per-mode super-shard row ranges, NCCL all_to_all_single remap + "
-                       "all_gather_into_tensor of updated factor rows",
+                       (f"dp{world}: per-mode super-shard row ranges; remap fused with the "
+                        "exchange (records stored into the owner GPU's buffer over NVLink peer "
+                        "memory, CUDA IPC) + peer pull of updated factor rows"
+                        if exchange == "p2p" else
+                        f"dp{world}: per-mode super-shard row ranges, NCCL all_to_all_single remap + "
+                        "all_gather_into_tensor of updated factor rows"),
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
                        "mode_ms": [round(1e3 * x, 4) for x in mode_secs[:N]]},

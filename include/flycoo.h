@@ -106,6 +106,42 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
                    int do_compute, int do_remap, int acc_in_smem,
                    int32_t *flags, unsigned long long *counters, void *stream);
 
+/* Multi-GPU mode pass with the remap fused with the exchange (dist.py,
+ * exchange "p2p"): same work plan and arguments as fc_mode_worker, but
+ * dest_slots hold GLOBAL mode-(n+1) positions and every record is stored
+ * straight into the back buffer of the GPU that owns its slot -- GPU q owns
+ * [peer_base[q], peer_base[q+1]) and its buffer is peer_crd[q] (peer_val[q]
+ * for N = 4 / N >= 5 separate values), an NVLink peer mapping from
+ * fc_ipc_open (or this GPU's own buffer).  Replaces the send-region pass,
+ * the NCCL all-to-all and fc_scatter_records.  npeers <= 8; nnz = local
+ * element count (remap-only pass); the caller orders the passes of all GPUs
+ * (barrier between modes). */
+int fc_mode_worker_peers(const void *src_crd, const float *src_val,
+                         const float *const *factors, const int64_t *dims,
+                         float *out, int nmodes, int mode, int rank,
+                         int64_t out_rows, int64_t m_mode,
+                         const int64_t *chunk_start, const int32_t *chunk_ss,
+                         const int32_t *chunk_part, const int32_t *chunk_rows,
+                         int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                         const int64_t *red1, int64_t nred1, const int64_t *red2,
+                         int64_t nred2, float *part_ws, float *part_ws2,
+                         const uint32_t *dest_slots, int64_t nnz, int do_compute,
+                         int acc_in_smem, int32_t *flags, unsigned long long *counters,
+                         int npeers, void *const *peer_crd, float *const *peer_val,
+                         const int64_t *peer_base, void *stream);
+
+/* Peer-memory plumbing for the fused exchange (no reference counterpart:
+ * the reference is single-node shared memory).  IPC-shareable cudaMalloc
+ * allocations, their fc_ipc_handle_bytes()-byte handles, peer mappings and
+ * stream-ordered copies (cudaMemcpyDefault: local or peer). */
+int fc_ipc_handle_bytes(void);
+int fc_ipc_alloc(int64_t bytes, void **ptr);
+int fc_ipc_free(void *ptr);
+int fc_ipc_handle(const void *ptr, void *handle);
+int fc_ipc_open(const void *handle, void **ptr);
+int fc_ipc_close(void *ptr);
+int fc_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Cursor remap strategy (_kernels.py:73-80): b = src_sid[i, next_mode];
  * slot = dest_base[b] + fetch_add(cursors[b]); dst[slot] = src[i] together
  * with the element's N shard ids (the reference carries sids in every

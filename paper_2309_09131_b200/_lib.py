@@ -42,6 +42,25 @@ _SIGS = {
         _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots, nnz
         _int, _int, _int,              # do_compute, do_remap, acc_in_smem
         _vp, _vp, _vp]),               # flags, counters, stream
+    "fc_mode_worker_peers": (_int, [
+        _vp, _vp,                      # src_crd, src_val
+        _vp, _vp, _vp,                 # factors (host array of device ptrs), dims (host), out
+        _int, _int, _int,              # nmodes, mode, rank
+        _i64, _i64,                    # out_rows, m_mode
+        _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks
+        _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
+        _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots (global), nnz (local)
+        _int, _int,                    # do_compute, acc_in_smem
+        _vp, _vp,                      # flags, counters
+        _int, _vp, _vp, _vp,           # npeers, peer_crd, peer_val (host arrays), peer_base (host)
+        _vp]),                         # stream
+    "fc_ipc_handle_bytes": (_int, []),
+    "fc_ipc_alloc": (_int, [_i64, _vp]),
+    "fc_ipc_free": (_int, [_vp]),
+    "fc_ipc_handle": (_int, [_vp, _vp]),
+    "fc_ipc_open": (_int, [_vp, _vp]),
+    "fc_ipc_close": (_int, [_vp]),
+    "fc_copy_async": (_int, [_vp, _vp, _i64, _vp]),
     "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),
     "fc_scatter_records": (_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _int, _vp, _vp, _vp]),
     "fc_build_morton": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),

@@ -35,37 +35,41 @@ inline bool pack_enabled() {
   return v == 1;
 }
 
-template <int NM, int MODE, int LPG, int RT>
+template <int NM, int MODE, int LPG, int RT, bool PEER>
 int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   if constexpr (NM == 3) {
     // 8-byte sorted records when the two input coordinates fit 32 bits
-    if (a.pack_shift > 0 && kernel_kind() == 1 && pack_enabled())
-      return launch_pack<MODE, LPG, RT>(a, nchunks, st);
+    if (a.pack_shift > 0 && (PEER || kernel_kind() == 1) && pack_enabled())
+      return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
   }
-  // direct chunks (hist_rows > tile_rows) exist only in the tile kernel
-  if (a.hist_rows > a.tile_rows) return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
-  switch (kernel_kind()) {
-    case 1: return launch_fast<NM, MODE, LPG, RT>(a, nchunks, st);
-    case 2: return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);
-    default: return launch_warp<NM, MODE, LPG, RT>(a, nchunks, st);
+  // multi-GPU fused exchange: tile kernel only; direct chunks (hist_rows >
+  // tile_rows) exist only in the tile kernel
+  if (PEER || a.hist_rows > a.tile_rows) return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
+  if constexpr (!PEER) {
+    switch (kernel_kind()) {
+      case 2: return launch_pipe<NM, MODE, LPG, RT>(a, nchunks, st);
+      case 0: return launch_warp<NM, MODE, LPG, RT>(a, nchunks, st);
+      default: break;
+    }
   }
+  return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
 }
 
-template <int NM, int MODE>
+template <int NM, int MODE, bool PEER>
 int dispatch_fast_mode(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  if (a.rank == 32) return launch_choice<NM, MODE, 8, 32>(a, nchunks, st);
-  if (a.rank == 16) return launch_choice<NM, MODE, 4, 16>(a, nchunks, st);
-  return launch_choice<NM, MODE, 16, 0>(a, nchunks, st);  // any R % 4 == 0 up to 64
+  if (a.rank == 32) return launch_choice<NM, MODE, 8, 32, PEER>(a, nchunks, st);
+  if (a.rank == 16) return launch_choice<NM, MODE, 4, 16, PEER>(a, nchunks, st);
+  return launch_choice<NM, MODE, 16, 0, PEER>(a, nchunks, st);  // any R % 4 == 0 up to 64
 }
 
-template <int NM>
+template <int NM, bool PEER = false>
 int dispatch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   switch (a.mode) {
-    case 0: return dispatch_fast_mode<NM, 0>(a, nchunks, st);
-    case 1: return dispatch_fast_mode<NM, 1>(a, nchunks, st);
-    case 2: if constexpr (NM > 2) return dispatch_fast_mode<NM, (NM > 2 ? 2 : 0)>(a, nchunks, st);
+    case 0: return dispatch_fast_mode<NM, 0, PEER>(a, nchunks, st);
+    case 1: return dispatch_fast_mode<NM, 1, PEER>(a, nchunks, st);
+    case 2: if constexpr (NM > 2) return dispatch_fast_mode<NM, (NM > 2 ? 2 : 0), PEER>(a, nchunks, st);
             break;
-    case 3: if constexpr (NM > 3) return dispatch_fast_mode<NM, (NM > 3 ? 3 : 0)>(a, nchunks, st);
+    case 3: if constexpr (NM > 3) return dispatch_fast_mode<NM, (NM > 3 ? 3 : 0), PEER>(a, nchunks, st);
             break;
     default: break;
   }

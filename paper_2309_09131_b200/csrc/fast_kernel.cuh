@@ -94,6 +94,40 @@ __device__ __forceinline__ void element_prod(const ModeArgs &a, int R, int col, 
   }
 }
 
+// Factor bases of the N-1 input modes with the lane's column offset folded
+// in, built once per tile so phase C does not re-derive them per element.
+template <int NM, int MODE>
+struct FacBases {
+  const float *p[NM > 1 ? NM - 1 : 1];
+  uint32_t stride;
+  __device__ __forceinline__ FacBases(const ModeArgs &a, int R, int col) : stride((uint32_t)R) {
+    int k = 0;
+#pragma unroll
+    for (int w = 0; w < NM; ++w) {
+      if (w == MODE) continue;
+      p[k++] = a.fac[w] + col;
+    }
+  }
+};
+
+template <int NM, int MODE>
+__device__ __forceinline__ void element_prod(const FacBases<NM, MODE> &fb, const int4 &q,
+                                             float (&pr)[4]) {
+  int k = 0;
+#pragma unroll
+  for (int w = 0; w < NM; ++w) {
+    if (w == MODE) continue;
+    const int c = w == 0 ? q.x : w == 1 ? q.y : w == 2 ? q.z : q.w;
+    const float4 f = __ldg(reinterpret_cast<const float4 *>(fb.p[k] + (uint64_t)(uint32_t)c * fb.stride));
+    if (k == 0) {
+      pr[0] = f.x; pr[1] = f.y; pr[2] = f.z; pr[3] = f.w;
+    } else {
+      pr[0] *= f.x; pr[1] *= f.y; pr[2] *= f.z; pr[3] *= f.w;
+    }
+    ++k;
+  }
+}
+
 // Reference-compatible name used by the pipeline kernel: t = v * prod.
 template <int NM, int MODE, int RT>
 __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, const int4 &q,
@@ -104,8 +138,8 @@ __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, 
   for (int k = 0; k < 4; ++k) t[k] = v * pr[k];
 }
 
-template <int NM, int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const ModeArgs a) {
+template <int NM, int MODE, int LPG, int RT, bool PEER = false>
+__global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const __grid_constant__ ModeArgs a) {
   using FP = FastPlan<NM, LPG>;
   constexpr int G = FP::G;
   constexpr int P = FP::P;
@@ -194,13 +228,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       const int e = j * kFBlock + tid;
       if (e < cnt) {
         if (a.do_remap) {
-          const uint64_t s = slot[j];
-          if (s < (uint64_t)a.nnz) {
-            a.dst[s] = rec[j];
-            if (!EMB) a.dst_val[s] = rv[j];
-          } else {
-            atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
-          }
+          remap_store<1, EMB, PEER>(a, slot[j], rec[j], rec[j], EMB ? 0.f : rv[j]);
         }
         if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
       }
@@ -345,6 +373,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       // positions of one piece share the pad: phys(p) = p + gi for p in [pb, pb + P)
       const int4 *sp = s_sorted + gi;
       const float *svp = s_sval + gi;
+      const FacBases<NM, MODE> fb(a, RT > 0 ? RT : R, col);
       int p = pb;
 #ifdef FAST_SWP
       // software pipeline (distance 1): block b+1's record loads and gathers
@@ -361,7 +390,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
           }
           if (col_ok) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) element_prod<NM, MODE, RT>(a, R, col, q[u], pr[u]);
+            for (int u = 0; u < U; ++u) element_prod(fb, q[u], pr[u]);
           }
         };
         fetch(p, qa, va, pa);
@@ -394,7 +423,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         float pr[U][4];
         if (col_ok) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) element_prod<NM, MODE, RT>(a, R, col, q[u], pr[u]);
+          for (int u = 0; u < U; ++u) element_prod(fb, q[u], pr[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
@@ -404,7 +433,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         const int4 q = sp[p];
         const float vv = EMB ? __int_as_float(q.w) : svp[p];
         float pr[4];
-        if (col_ok) element_prod<NM, MODE, RT>(a, R, col, q, pr);
+        if (col_ok) element_prod(fb, q, pr);
         consume(comp<MODE>(q), vv, pr);
       }
       const bool tail = pe < nvalid && comp<MODE>(s_sorted[phys(pe)]) == cur;
@@ -486,10 +515,10 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #endif
 }
 
-template <int NM, int MODE, int LPG, int RT>
+template <int NM, int MODE, int LPG, int RT, bool PEER = false>
 int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT>;
+  auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT, PEER>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

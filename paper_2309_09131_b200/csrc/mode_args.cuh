@@ -10,6 +10,18 @@ constexpr int kIPT = 8;
 constexpr int kTile = kBlock * kIPT;  // 2048 elements per tile
 constexpr int64_t kSmemAccBytes = 64 * 1024;
 
+// Multi-GPU fused exchange: the remap stores every record straight into
+// the back buffer of the GPU that owns its next-mode slot, through NVLink
+// peer memory (CUDA IPC mappings).  Slots are global mode-(n+1) positions;
+// GPU q owns [base[q], base[q + 1]).  n == 0: single-GPU (dst / nnz).
+constexpr int kMaxPeers = 8;
+struct PeerTable {
+  int n;
+  int4 *crd[kMaxPeers];
+  float *val[kMaxPeers];
+  int64_t base[kMaxPeers + 1];
+};
+
 struct ModeArgs {
   const int4 *src;
   const float *src_val;
@@ -33,7 +45,41 @@ struct ModeArgs {
   int do_remap;
   int32_t *flags;
   unsigned long long *counters;
+  PeerTable peers;
 };
+
+// Remap store of one record (CW4 16-byte words + optional separate value)
+// to slot s: this GPU's back buffer, or the owning peer's.  Out-of-range
+// slots raise FC_FLAG_SLOT_RANGE.
+// Remap store of one record (CW4 16-byte words + optional separate value)
+// to slot s: this GPU's back buffer, or -- PEER, multi-GPU fused exchange --
+// the back buffer of the GPU owning s (peer table; compile-time so the
+// single-GPU kernels keep their registers).  Out-of-range slots raise
+// FC_FLAG_SLOT_RANGE.
+template <int CW4, bool EMB, bool PEER = false>
+__device__ __forceinline__ void remap_store(const ModeArgs &a, uint64_t s, const int4 &r0,
+                                            const int4 &r1, float v) {
+  int4 *d = a.dst;
+  float *dv = a.dst_val;
+  uint64_t cap = (uint64_t)a.nnz;
+  if (PEER) {
+    int q = 0;
+#pragma unroll
+    for (int k = 1; k < kMaxPeers; ++k) q += (k < a.peers.n && s >= (uint64_t)a.peers.base[k]);
+    const uint64_t b = (uint64_t)a.peers.base[q];
+    cap = (uint64_t)a.peers.base[q + 1] - b;
+    s -= b;  // base[0] = 0: no wrap
+    d = a.peers.crd[q];
+    dv = a.peers.val[q];
+  }
+  if (s < cap) {
+    d[s * CW4] = r0;
+    if (CW4 == 2) d[s * CW4 + 1] = r1;
+    if (!EMB) dv[s] = v;
+  } else {
+    atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
+  }
+}
 
 // chunk_part value of a direct chunk: whole super-shards within one tile,
 // rows stored straight to `out` (fast tile kernel only)
@@ -121,5 +167,9 @@ constexpr int kWarps = kBlock / 32;
 int fast_dispatch_n2(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 int fast_dispatch_n3(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 int fast_dispatch_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+// peer-store (multi-GPU fused exchange) instances, fast_n*_peer.cu
+int fast_dispatch_peer_n2(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+int fast_dispatch_peer_n3(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
+int fast_dispatch_peer_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 
 }  // namespace fc

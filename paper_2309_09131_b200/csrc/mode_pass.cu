@@ -55,7 +55,7 @@ struct SmemPlan {
 // NM_T: number of modes (0 = runtime, up to 8).  VEC/LPG: columns per lane /
 // lanes per element group.  MAXIT: column blocks of LPG*VEC per group.
 template <int NM_T, int VEC, int LPG, int MAXIT, bool SMEM_ACC>
-__global__ void __launch_bounds__(kBlock) mode_pass_kernel(const ModeArgs a) {
+__global__ void __launch_bounds__(kBlock) mode_pass_kernel(const __grid_constant__ ModeArgs a) {
   constexpr int NMAX = NM_T > 0 ? NM_T : 8;
   constexpr int CW4 = NM_T > 0 ? crd_words(NM_T) / 4 : 2;  // runtime NM: room for 8 words
   constexpr bool EMB_T = NM_T > 0 ? value_embedded(NM_T) : false;
@@ -138,13 +138,18 @@ __global__ void __launch_bounds__(kBlock) mode_pass_kernel(const ModeArgs a) {
       vals16[j] = (uint16_t)e;
       if (e < cnt) {
         if (a.do_remap) {
-          const uint64_t s = slot[j];
-          if (s < (uint64_t)a.nnz) {
-            a.dst[s * cw4] = r0[j];
-            if (CW4 == 2 && cw4 == 2) a.dst[s * cw4 + 1] = r1[j];
-            if (!emb) a.dst_val[s] = rv[j];
+          // general kernel (N >= 5, R > 64): peer test at run time
+          const bool two = CW4 == 2 && cw4 == 2;
+          if (a.peers.n > 0) {
+            if (two && emb) remap_store<2, true, true>(a, slot[j], r0[j], r1[j], 0.f);
+            else if (two) remap_store<2, false, true>(a, slot[j], r0[j], r1[j], rv[j]);
+            else if (emb) remap_store<1, true, true>(a, slot[j], r0[j], r1[j], 0.f);
+            else remap_store<1, false, true>(a, slot[j], r0[j], r1[j], rv[j]);
           } else {
-            atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
+            if (two && emb) remap_store<2, true>(a, slot[j], r0[j], r1[j], 0.f);
+            else if (two) remap_store<2, false>(a, slot[j], r0[j], r1[j], rv[j]);
+            else if (emb) remap_store<1, true>(a, slot[j], r0[j], r1[j], 0.f);
+            else remap_store<1, false>(a, slot[j], r0[j], r1[j], rv[j]);
           }
         }
         s_rec[e * CW4] = r0[j];
@@ -367,29 +372,23 @@ __global__ void __launch_bounds__(256) reduce_level_kernel(const int64_t *tasks,
   else slots[dst * cells + idx] = s;
 }
 
-// Remap-only pass (split_remap second pass, engine.py:312).
+// Remap-only pass (split_remap second pass, engine.py:312) of n elements;
+// also the receiver unpack of the NCCL exchange (fc_scatter_records).
 template <int CW4, bool EMB>
-__global__ void __launch_bounds__(256) remap_only_kernel(const int4 *src, const float *src_val,
-                                                         int4 *dst, float *dst_val,
-                                                         const uint32_t *slots, int64_t n,
-                                                         int64_t dst_cap, int32_t *flags,
-                                                         unsigned long long *counters) {
+__global__ void __launch_bounds__(256) remap_only_kernel(const __grid_constant__ ModeArgs a, int64_t n) {
   unsigned done = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t s = ld_stream_u32(slots + i);
-    if (s >= (uint64_t)dst_cap) {
-      atomicOr(flags, FC_FLAG_SLOT_RANGE);
-      ++done;
-      continue;
-    }
-#pragma unroll
-    for (int q = 0; q < CW4; ++q) dst[s * CW4 + q] = ld_stream_v4(src + i * CW4 + q);
-    if (!EMB) dst_val[s] = ld_stream_f32(src_val + i);
+    const uint64_t s = ld_stream_u32(a.slots + i);
+    const int4 r0 = ld_stream_v4(a.src + i * CW4);
+    const int4 r1 = CW4 == 2 ? ld_stream_v4(a.src + i * CW4 + 1) : r0;
+    const float v = EMB ? 0.f : ld_stream_f32(a.src_val + i);
+    if (a.peers.n > 0) remap_store<CW4, EMB, true>(a, s, r0, r1, v);
+    else remap_store<CW4, EMB>(a, s, r0, r1, v);
     ++done;
   }
   done = __reduce_add_sync(0xffffffffu, done);
-  if ((threadIdx.x & 31) == 0 && done) atomicAdd(counters, (unsigned long long)done);
+  if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.counters, (unsigned long long)done);
 }
 
 // Cursor strategy (_kernels.py:73-80).
@@ -449,6 +448,11 @@ int dispatch(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const int R = a.rank;
   const int N = a.nmodes;
   if (fast_ok(a, SMEM_ACC)) {
+    if (a.peers.n > 0) {
+      if (N == 3) return fast_dispatch_peer_n3(a, nchunks, st);
+      if (N == 4) return fast_dispatch_peer_n4(a, nchunks, st);
+      return fast_dispatch_peer_n2(a, nchunks, st);
+    }
     if (N == 3) return fast_dispatch_n3(a, nchunks, st);
     if (N == 4) return fast_dispatch_n4(a, nchunks, st);
     return fast_dispatch_n2(a, nchunks, st);
@@ -484,23 +488,23 @@ int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m) {
   return kMaxBins / m * m;
 }
 
-int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
-                   const float *const *factors, const int64_t *dims, float *out, int nmodes,
-                   int mode, int rank,
-                   int64_t out_rows, int64_t m_mode, const int64_t *chunk_start,
-                   const int32_t *chunk_ss, const int32_t *chunk_part,
-                   const int32_t *chunk_rows, int64_t tile_rows, int64_t hist_rows,
-                   int64_t nchunks,
-                   const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
-                   float *part_ws, float *part_ws2, const uint32_t *dest_slots, int64_t nnz,
-                   int do_compute,
-                   int do_remap, int acc_in_smem, int32_t *flags, unsigned long long *counters,
-                   void *stream) {
+static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst_crd,
+                            float *dst_val, const float *const *factors, const int64_t *dims,
+                            float *out, int nmodes, int mode, int rank, int64_t out_rows,
+                            int64_t m_mode, const int64_t *chunk_start, const int32_t *chunk_ss,
+                            const int32_t *chunk_part, const int32_t *chunk_rows,
+                            int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                            const int64_t *red1, int64_t nred1, const int64_t *red2,
+                            int64_t nred2, float *part_ws, float *part_ws2,
+                            const uint32_t *dest_slots, int64_t nnz, int do_compute,
+                            int do_remap, int acc_in_smem, int32_t *flags,
+                            unsigned long long *counters, void *stream, const PeerTable &peers) {
   FC_CHECK_ARG(nmodes >= 2 && nmodes <= 8, "nmodes %d outside [2, 8]", nmodes);
   FC_CHECK_ARG(mode >= 0 && mode < nmodes, "mode %d out of range", mode);
   FC_CHECK_ARG(src_crd && flags && counters, "null buffer");
-  FC_CHECK_ARG(!do_remap || (dst_crd && dest_slots), "remap needs dst and slots");
-  FC_CHECK_ARG(value_embedded(nmodes) || (src_val && (!do_remap || dst_val)),
+  FC_CHECK_ARG(!do_remap || ((dst_crd || peers.n > 0) && (dest_slots || nnz == 0)),
+               "remap needs dst and slots");
+  FC_CHECK_ARG(value_embedded(nmodes) || (src_val && (!do_remap || dst_val || peers.n > 0)),
                "N=%d needs separate value arrays", nmodes);
   FC_CHECK_ARG(nnz >= 0 && nnz <= (int64_t)UINT32_MAX, "nnz %lld outside uint32 slots",
                (long long)nnz);
@@ -510,16 +514,20 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
   if (!do_compute) {
     if (!do_remap || nnz == 0) return FC_OK;
     const int grid = (int)min64((nnz + 255) / 256, 148 * 16);
-    auto src4 = static_cast<const int4 *>(src_crd);
-    auto dst4 = static_cast<int4 *>(dst_crd);
-    if (cw4 == 1 && emb)
-      remap_only_kernel<1, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
-    else if (cw4 == 1)
-      remap_only_kernel<1, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
-    else if (emb)
-      remap_only_kernel<2, true><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
-    else
-      remap_only_kernel<2, false><<<grid, 256, 0, st>>>(src4, src_val, dst4, dst_val, dest_slots, nnz, nnz, flags, counters);
+    ModeArgs r{};
+    r.src = static_cast<const int4 *>(src_crd);
+    r.src_val = src_val;
+    r.dst = static_cast<int4 *>(dst_crd);
+    r.dst_val = dst_val;
+    r.slots = dest_slots;
+    r.nnz = nnz;
+    r.flags = flags;
+    r.counters = counters;
+    r.peers = peers;
+    if (cw4 == 1 && emb) remap_only_kernel<1, true><<<grid, 256, 0, st>>>(r, nnz);
+    else if (cw4 == 1) remap_only_kernel<1, false><<<grid, 256, 0, st>>>(r, nnz);
+    else if (emb) remap_only_kernel<2, true><<<grid, 256, 0, st>>>(r, nnz);
+    else remap_only_kernel<2, false><<<grid, 256, 0, st>>>(r, nnz);
     FC_LAUNCH_CHECK();
     return FC_OK;
   }
@@ -570,6 +578,7 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
   a.do_remap = do_remap;
   a.flags = flags;
   a.counters = counters;
+  a.peers = peers;
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
   if (acc_in_smem && nred1 > 0) {
@@ -588,6 +597,57 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
     }
   }
   return FC_OK;
+}
+
+int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
+                   const float *const *factors, const int64_t *dims, float *out, int nmodes,
+                   int mode, int rank, int64_t out_rows, int64_t m_mode,
+                   const int64_t *chunk_start, const int32_t *chunk_ss,
+                   const int32_t *chunk_part, const int32_t *chunk_rows, int64_t tile_rows,
+                   int64_t hist_rows, int64_t nchunks, const int64_t *red1, int64_t nred1,
+                   const int64_t *red2, int64_t nred2, float *part_ws, float *part_ws2,
+                   const uint32_t *dest_slots, int64_t nnz, int do_compute, int do_remap,
+                   int acc_in_smem, int32_t *flags, unsigned long long *counters, void *stream) {
+  PeerTable none{};
+  return mode_worker_impl(src_crd, src_val, dst_crd, dst_val, factors, dims, out, nmodes, mode,
+                          rank, out_rows, m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows,
+                          tile_rows, hist_rows, nchunks, red1, nred1, red2, nred2, part_ws,
+                          part_ws2, dest_slots, nnz, do_compute, do_remap, acc_in_smem, flags,
+                          counters, stream, none);
+}
+
+int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float *const *factors,
+                         const int64_t *dims, float *out, int nmodes, int mode, int rank,
+                         int64_t out_rows, int64_t m_mode, const int64_t *chunk_start,
+                         const int32_t *chunk_ss, const int32_t *chunk_part,
+                         const int32_t *chunk_rows, int64_t tile_rows, int64_t hist_rows,
+                         int64_t nchunks, const int64_t *red1, int64_t nred1,
+                         const int64_t *red2, int64_t nred2, float *part_ws, float *part_ws2,
+                         const uint32_t *dest_slots, int64_t nnz, int do_compute,
+                         int acc_in_smem, int32_t *flags, unsigned long long *counters,
+                         int npeers, void *const *peer_crd, float *const *peer_val,
+                         const int64_t *peer_base, void *stream) {
+  FC_CHECK_ARG(npeers >= 1 && npeers <= kMaxPeers, "npeers %d outside [1, %d]", npeers, kMaxPeers);
+  FC_CHECK_ARG(peer_crd && peer_base && (dest_slots || nnz == 0), "null peer table");
+  PeerTable t{};
+  t.n = npeers;
+  FC_CHECK_ARG(peer_base[0] == 0, "peer_base[0] must be 0");
+  for (int q = 0; q < npeers; ++q) {
+    FC_CHECK_ARG(peer_crd[q], "null peer buffer %d", q);
+    FC_CHECK_ARG(value_embedded(nmodes) || (peer_val && peer_val[q]), "null peer values %d", q);
+    FC_CHECK_ARG(peer_base[q + 1] >= peer_base[q], "peer_base not monotone");
+    t.crd[q] = static_cast<int4 *>(peer_crd[q]);
+    t.val[q] = value_embedded(nmodes) ? nullptr : peer_val[q];
+    t.base[q] = peer_base[q];
+  }
+  t.base[npeers] = peer_base[npeers];
+  for (int q = npeers + 1; q <= kMaxPeers; ++q) t.base[q] = t.base[npeers];
+  FC_CHECK_ARG(t.base[npeers] <= (int64_t)UINT32_MAX + 1, "global slots exceed uint32");
+  return mode_worker_impl(src_crd, src_val, nullptr, nullptr, factors, dims, out, nmodes, mode,
+                          rank, out_rows, m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows,
+                          tile_rows, hist_rows, nchunks, red1, nred1, red2, nred2, part_ws,
+                          part_ws2, dest_slots, nnz, do_compute, 1, acc_in_smem, flags, counters,
+                          stream, t);
 }
 
 int fc_remap_cursor(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
@@ -629,16 +689,19 @@ int fc_scatter_records(const void *src_crd, const float *src_val, int64_t n, voi
   if (n == 0) return FC_OK;
   cudaStream_t st = as_stream(stream);
   const int grid = (int)min64((n + 255) / 256, 148 * 16);
-  auto s4 = static_cast<const int4 *>(src_crd);
-  auto d4 = static_cast<int4 *>(dst_crd);
-  if (cw4 == 1 && emb)
-    remap_only_kernel<1, true><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
-  else if (cw4 == 1)
-    remap_only_kernel<1, false><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
-  else if (emb)
-    remap_only_kernel<2, true><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
-  else
-    remap_only_kernel<2, false><<<grid, 256, 0, st>>>(s4, src_val, d4, dst_val, slots, n, dst_capacity, flags, counters);
+  ModeArgs r{};
+  r.src = static_cast<const int4 *>(src_crd);
+  r.src_val = src_val;
+  r.dst = static_cast<int4 *>(dst_crd);
+  r.dst_val = dst_val;
+  r.slots = slots;
+  r.nnz = dst_capacity;
+  r.flags = flags;
+  r.counters = counters;
+  if (cw4 == 1 && emb) remap_only_kernel<1, true><<<grid, 256, 0, st>>>(r, n);
+  else if (cw4 == 1) remap_only_kernel<1, false><<<grid, 256, 0, st>>>(r, n);
+  else if (emb) remap_only_kernel<2, true><<<grid, 256, 0, st>>>(r, n);
+  else remap_only_kernel<2, false><<<grid, 256, 0, st>>>(r, n);
   FC_LAUNCH_CHECK();
   return FC_OK;
 }

@@ -40,8 +40,8 @@ struct PackPlan {
   }
 };
 
-template <int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const ModeArgs a) {
+template <int MODE, int LPG, int RT, bool PEER = false>
+__global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const __grid_constant__ ModeArgs a) {
   using PP = PackPlan<LPG>;
   constexpr int G = PP::G;
   constexpr int P = PP::P;
@@ -122,9 +122,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       const int e = j * kFBlock + tid;
       if (e < cnt) {
         if (a.do_remap) {
-          const uint64_t s = slot[j];
-          if (s < (uint64_t)a.nnz) a.dst[s] = rec[j];
-          else atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
+          remap_store<1, true, PEER>(a, slot[j], rec[j], rec[j], 0.f);
         }
         if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
       }
@@ -348,10 +346,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 }
 
-template <int MODE, int LPG, int RT>
+template <int MODE, int LPG, int RT, bool PEER = false>
 int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = PackPlan<LPG>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_pack_kernel<MODE, LPG, RT>;
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -71,7 +71,7 @@ struct PipePlan {
 };
 
 template <int NM, int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const ModeArgs a,
+__global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const __grid_constant__ ModeArgs a,
                                                                          int64_t nchunks) {
   using PP = PipePlan<NM, LPG>;
   constexpr int G = PP::G;
@@ -139,13 +139,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) mode_pass_pipe_kernel(const M
           const int e = j * kProdThreads + tid;
           if (e < cnt) {
             if (a.do_remap) {
-              const uint64_t s = slot[j];
-              if (s < (uint64_t)a.nnz) {
-                a.dst[s] = rec[j];
-                if (!EMB) a.dst_val[s] = rv[j];
-              } else {
-                atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
-              }
+              remap_store<1, EMB>(a, slot[j], rec[j], rec[j], EMB ? 0.f : rv[j]);
             }
             if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
           }

@@ -51,7 +51,7 @@ struct WarpPlan {
 };
 
 template <int NM, int MODE, int LPG, int RT>
-__global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const ModeArgs a) {
+__global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const __grid_constant__ ModeArgs a) {
   using WP = WarpPlan<NM, LPG>;
   constexpr int G = WP::G;
   constexpr int P = WP::P;
@@ -120,13 +120,7 @@ __global__ void __launch_bounds__(kWKThreads, 4) mode_pass_warp_kernel(const Mod
       const int e = j * 32 + lane;
       if (e < cnt) {
         if (a.do_remap) {
-          const uint64_t s = slot[j];
-          if (s < (uint64_t)a.nnz) {
-            a.dst[s] = rec[j];
-            if (!EMB) a.dst_val[s] = rv[j];
-          } else {
-            atomicOr(a.flags, FC_FLAG_SLOT_RANGE);
-          }
+          remap_store<1, EMB>(a, slot[j], rec[j], rec[j], EMB ? 0.f : rv[j]);
         }
         if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
       }

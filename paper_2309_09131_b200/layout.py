@@ -234,7 +234,8 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
                         PART_DIRECT).astype(np.int32)
         nparts = int(part_base[-1])
         r1, r2, nslots = reduce_plan(nch_ss, part_base)
-        ws = torch.empty(nparts * m * rank, dtype=torch.float32, device=dev) if nparts else None
+        ws = (torch.empty(max(nparts * m * rank, 1), dtype=torch.float32, device=dev)
+              if nparts or r1.shape[0] else None)
         ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
         return ModeWork(True, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), t(rows),
                         m, int(rows.max()) if rows.size else m, t(r1), int(r1.shape[0]), t(r2),
@@ -264,7 +265,10 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
         nparts, nslots = 0, 0
         r1 = np.zeros((0, 4), dtype=np.int64)
         r2 = np.zeros((0, 3), dtype=np.int64)
-    ws = torch.empty(nparts * m * rank, dtype=torch.float32, device=dev) if nparts else None
+    # K2 also zeroes the rows of empty super-shards (tasks with no partials),
+    # so a plan can have reduce tasks but no partial tiles: 1-float workspace
+    ws = (torch.empty(max(nparts * m * rank, 1), dtype=torch.float32, device=dev)
+          if nparts or r1.shape[0] else None)
     ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
     return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), None, m, m,
                     t(r1), int(r1.shape[0]), t(r2), int(r2.shape[0]), nparts, ws, ws2, C)

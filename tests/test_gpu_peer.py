@@ -1,0 +1,139 @@
+"""Fused remap + exchange over peer memory (peer.py, fc_mode_worker_peers).
+
+1. Virtual ranks in one process on one GPU: every rank's pass stores its
+   records straight into the owners' back buffers through the peer table
+   (ordinary device allocations here); after every mode each rank's slice
+   must equal the single-GPU layout bit-exactly and the pulled factor must
+   equal the single-GPU sweep's.
+2. Two processes sharing the GPU through CUDA IPC (gloo for the host-side
+   handle exchange and the barrier): the real mapping path.  The ranks'
+   kernels never wait on each other -- the barrier is on the host.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(N, nnz=400_000):
+    from paper_2309_09131_b200 import build_device_sharded, device_params
+    from paper_2309_09131_b200.synth import zipf_tensor
+    dims = {3: (3000, 2000, 2500), 4: (300, 400, 250, 90), 5: (60, 50, 40, 30, 20)}[N]
+    coords, vals = zipf_tensor(dims, nnz, seed=6, exponents=(1.1,) * N)
+    params = device_params(dims, nnz, 32, g=4096, m=[16] * N)
+    return dims, coords, vals, params, build_device_sharded
+
+
+def _virtual_sweep(N, world, sweeps=2):
+    from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, schedule_super_shards
+    from paper_2309_09131_b200.peer import PeerShardedTensor
+    dims, coords, vals, params, build = _case(N)
+    st = build(coords, vals, params)
+    ref = build(coords, vals, params)
+    ranks = [PeerShardedTensor(st, world, r, ipc=False) for r in range(world)]
+    PeerShardedTensor.connect_local(ranks)
+    f0 = DeviceFactorSet.random(dims, 32, seed=3)
+    working = [list(f0.factors) for _ in range(world)]
+    ref_working = list(f0.factors)
+    smap = schedule_super_shards(ref.plan, 1)
+    for _ in range(sweeps):
+        for n in range(N):
+            outs = [dt.output(n, 32)[0] for dt in ranks]
+            for r, dt in enumerate(ranks):
+                dt.mode_pass(working[r], n, outs[r])
+            torch.cuda.synchronize()
+            ptrs = [o.data_ptr() for o in outs]
+            for r, dt in enumerate(ranks):
+                dt.pull_rows(n, outs[r], ptrs)
+                dt.swap()
+                working[r][n] = outs[r]
+            torch.cuda.synchronize()
+            ref_out = mttkrp_mode(ref, DeviceFactorSet(ref_working, None, validate=False), n, smap)
+            ref_working[n] = ref_out
+            nxt = (n + 1) % N
+            for r, dt in enumerate(ranks):
+                p = dt.plans[nxt]
+                got, gval = dt.local_records()
+                assert torch.equal(got, ref.crd[ref.active][p.e_lo:p.e_hi]), (world, N, n, r)
+                if gval is not None:
+                    assert torch.equal(gval, ref.val[ref.active][p.e_lo:p.e_hi]), (world, N, n, r)
+                # chunk grouping may differ at rank boundaries: fp32 reassociation only
+                assert torch.allclose(working[r][n], ref_out, rtol=1e-5, atol=0), (world, N, n, r)
+    for dt in ranks:
+        dt.check()
+
+
+@pytest.mark.parametrize("N", [3, 4, 5])
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_store_virtual_ranks(N, world):
+    torch.cuda.set_device(0)
+    _virtual_sweep(N, world)
+
+
+def test_peer_store_slot_out_of_range_flags():
+    """A global slot past the last owner's range raises the slot-range flag."""
+    from paper_2309_09131_b200 import DeviceFactorSet
+    from paper_2309_09131_b200.peer import PeerShardedTensor
+    dims, coords, vals, params, build = _case(3, 50_000)
+    st = build(coords, vals, params)
+    ranks = [PeerShardedTensor(st, 2, r, ipc=False) for r in range(2)]
+    PeerShardedTensor.connect_local(ranks)
+    ranks[0].plans[0].global_slots[5] = -2  # 0xFFFFFFFE
+    f = list(DeviceFactorSet.random(dims, 32, seed=1).factors)
+    out = ranks[0].output(0, 32)[0]
+    ranks[0].mode_pass(f, 0, out)
+    with pytest.raises(RuntimeError, match="flags 0x1"):
+        ranks[0].check()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, schedule_super_shards
+        from paper_2309_09131_b200.peer import PeerShardedTensor, peer_sweep_all_modes
+        for N in (3, 4):
+            dims, coords, vals, params, build = _case(N)
+            st = build(coords, vals, params)
+            ref = build(coords, vals, params)
+            dt = PeerShardedTensor(st, world, rank)
+            dt.connect()
+            f0 = DeviceFactorSet.random(dims, 32, seed=3)
+            got = peer_sweep_all_modes(dt, list(f0.factors))
+            ref_working = list(f0.factors)
+            smap = schedule_super_shards(ref.plan, 1)
+            for n in range(N):
+                ref_working[n] = mttkrp_mode(ref, DeviceFactorSet(ref_working, None, validate=False),
+                                             n, smap)
+            for n in range(N):
+                assert torch.allclose(got[n], ref_working[n], rtol=1e-5, atol=0), (rank, N, n)
+            p = dt.plans[0]
+            c, v = dt.local_records()
+            assert torch.equal(c, ref.crd[ref.active][p.e_lo:p.e_hi]), (rank, N)
+            dt.barrier()
+            dt.close()
+            dist.barrier()
+        result[rank] = 1
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_two_processes_ipc():
+    ctx = mp.get_context("spawn")
+    result = ctx.Manager().dict()
+    mp.start_processes(_ipc_worker, args=(2, _free_port(), result), nprocs=2, join=True,
+                       start_method="spawn")
+    assert sorted(result.keys()) == [0, 1]

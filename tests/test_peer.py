@@ -1,0 +1,105 @@
+"""Host logic of the fused remap + exchange (peer.py) on CPU: virtual ranks
+in one process, the device store emulated with torch exactly as
+``remap_store`` resolves it (owner q from the peer bounds, local position
+d - E'_q).  Every rank's slice after every mode must equal the single-GPU
+layout, and the pulled factors must equal the single-process sweep (oracle
+reference_mttkrp).  The CUDA path is tests/test_gpu_peer.py."""
+import types
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2309_09131_b200.peer import PeerShardedTensor, peer_plans
+from test_dist import _case, _global_records
+
+
+def _emulated_pass(ranks, r, factors, mode, out):
+    """K1 of virtual rank r: owned rows of `out` + peer stores."""
+    dt = ranks[r]
+    p = dt.plans[mode]
+    a, b = dt.active, 1 - dt.active
+    recs = dt.crd[a][:p.count]
+    N = dt.num_modes
+    v = recs[:, 3].view(torch.float32).double() if dt.val[a] is None else dt.val[a][:p.count].double()
+    t = v[:, None].clone()
+    for w in range(N):
+        if w != mode:
+            t = t * factors[w][recs[:, w].long()]
+    lo, hi = dt.owned_rows(mode)
+    out[lo:hi] = 0
+    out.index_add_(0, recs[:, mode].long(), t.to(out.dtype))
+    d = p.global_slots.long() & 0xFFFFFFFF
+    base = torch.tensor(p.peer_base)
+    q = torch.searchsorted(base, d, right=True) - 1
+    assert bool(((q >= 0) & (q < dt.world)).all())
+    for qq in range(dt.world):
+        sel = q == qq
+        l = d[sel] - base[qq]
+        ranks[qq].crd[b][l] = recs[sel]
+        if dt.val[b] is not None:
+            ranks[qq].val[b][l] = dt.val[a][:p.count][sel]
+
+
+@pytest.mark.parametrize("world,N", [(2, 3), (3, 3), (2, 4), (4, 3)])
+def test_peer_sweep_virtual_ranks_cpu(world, N):
+    dims, subs, vals, params, L, d, plan = _case(N)
+    rec0, val0 = _global_records(subs, vals, d.orders[0], N)
+    st = types.SimpleNamespace(
+        plan=plan, device=torch.device("cpu"), num_modes=N, active=0,
+        slot_maps=[torch.from_numpy(s.astype(np.int64)) for s in d.slot_maps],
+        crd=[torch.from_numpy(rec0), None],
+        val=[None if val0 is None else torch.from_numpy(val0), None])
+    ranks = [PeerShardedTensor(st, world, r, ipc=False) for r in range(world)]
+    rng = np.random.default_rng(9)
+    f0 = [torch.from_numpy(rng.random((dd, 8))) for dd in dims]
+    working = [list(f0) for _ in range(world)]
+    outs = {n: [torch.zeros((dims[n], 8), dtype=torch.float64) for _ in range(world)]
+            for n in range(N)}
+    for n in range(N):
+        for r in range(world):
+            _emulated_pass(ranks, r, working[r], n, outs[n][r])
+        for r, dt in enumerate(ranks):
+            # the pull: peers' owned rows into this rank's output
+            for q, (lo, hi) in enumerate(dt.row_ranges(n)):
+                if q != r:
+                    outs[n][r][lo:hi] = outs[n][q][lo:hi]
+            dt.swap()
+            working[r][n] = outs[n][r]
+        nxt = (n + 1) % N
+        want, wval = _global_records(subs, vals, d.orders[nxt], N)
+        for r, dt in enumerate(ranks):
+            p = dt.plans[nxt]
+            got, gval = dt.local_records()
+            assert np.array_equal(got.numpy(), want[p.e_lo:p.e_hi]), (r, n)
+            if wval is not None:
+                assert np.array_equal(gval.numpy(), wval[p.e_lo:p.e_hi]), (r, n)
+    ref = [f.numpy() for f in f0]
+    v64 = vals.astype(np.float32).astype(np.float64)
+    for n in range(N):
+        ref[n] = oracle.reference_mttkrp(subs, v64, ref, n)
+        for r in range(world):
+            np.testing.assert_allclose(working[r][n].numpy(), ref[n], rtol=1e-9, atol=0)
+
+
+def test_peer_plans_cover_every_slot_once():
+    dims, subs, vals, params, L, d, plan = _case(3)
+    slot_maps = [torch.from_numpy(s.astype(np.int64)) for s in d.slot_maps]
+    for world in (1, 2, 5, 8):
+        per_rank = [peer_plans(plan, slot_maps, world, r)[0] for r in range(world)]
+        for n in range(3):
+            base = per_rank[0][n].peer_base
+            assert len(base) == world + 1 and base[0] == 0 and base[-1] == len(vals)
+            allslots = torch.cat([pr[n].global_slots.long() for pr in per_rank])
+            assert torch.equal(torch.sort(allslots).values, torch.arange(len(vals)))
+            # every rank's bounds are the same static table
+            assert all(pr[n].peer_base == base for pr in per_rank)
+
+
+def test_peer_world_limit():
+    dims, subs, vals, params, L, d, plan = _case(3)
+    st = types.SimpleNamespace(plan=plan, device=torch.device("cpu"), num_modes=3, active=0,
+                               slot_maps=[torch.zeros(1)] * 3, crd=[None, None], val=[None, None])
+    with pytest.raises(ValueError, match="at most 8"):
+        PeerShardedTensor(st, 9, 0, ipc=False)
