@@ -2,6 +2,10 @@ import os
 import sys
 from pathlib import Path
 
+# the full-size tests (c4: 1.74B nonzeros) need the allocator to reuse freed
+# build scratch without fragmentation, as bench.py does
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 import numpy as np
 import pytest
 
