@@ -51,7 +51,7 @@ class SweepGraph:
         self.inputs = [f.clone() for f in fs.factors]
         self.N = st.num_modes
         self.pool = torch.cuda.graph_pool_handle()
-        self.graphs = {}      # active parity -> (CUDAGraph, outputs)
+        self.graphs = {}      # (active parity, host copies) -> (CUDAGraph, outputs)
         # eager sweeps first: caches every work plan and configures the kernels'
         # shared-memory attributes outside capture (results discarded)
         for _ in range(1 if self.N % 2 == 0 else 2):
@@ -59,42 +59,82 @@ class SweepGraph:
                                                 validate=False), smap)
         torch.cuda.synchronize()
 
-    def _capture(self):
+    def bind_host(self, host_in, host_out):
+        """Pinned host buffers for :meth:`run_host`: `host_in[w]` feeds input
+        factor w (only w >= 1 is read: mode 0's output replaces factor 0
+        before anything reads it), `host_out[n]` receives updated factor n.
+        The copies are part of the graph: each output's device-to-host copy
+        runs on a side stream while the later modes compute."""
+        for t in list(host_in) + list(host_out):
+            if not t.is_pinned():
+                raise ValueError("bind_host needs pinned host tensors")
+        self.host_in, self.host_out = list(host_in), list(host_out)
+        self.graphs = {k: v for k, v in self.graphs.items() if not k[1]}
+
+    def host_bytes(self):
+        """(h2d, d2h) bytes one run_host moves."""
+        return (sum(t.numel() * t.element_size() for t in self.host_in[1:]),
+                sum(t.numel() * t.element_size() for t in self.host_out))
+
+    def _capture(self, host: bool):
         st = self.st
         parity = st.active
         saved = (st.active, st.active_mode, st._expected)
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=st.device)
+        copies = torch.cuda.Stream(device=st.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, pool=self.pool, stream=side):
                 st._stat.zero_()
+                if host:
+                    for w in range(1, self.N):
+                        self.inputs[w].copy_(self.host_in[w], non_blocking=True)
                 working = list(self.inputs)
                 for n in range(self.N):
                     cur = DeviceFactorSet(tuple(working), self.lambdas, st.device, validate=False)
                     working[n] = mttkrp_mode(st, cur, n, self.smap, check=False)
+                    if host:  # fork: copy out mode n while the next modes run
+                        copies.wait_stream(side)
+                        with torch.cuda.stream(copies):
+                            self.host_out[n].copy_(working[n], non_blocking=True)
+                if host:
+                    side.wait_stream(copies)  # join
         torch.cuda.current_stream().wait_stream(side)
         # capture ran the host side once: restore the tensor's host state
         st.active, st.active_mode, st._expected = saved
-        self.graphs[parity] = (g, working)
+        self.graphs[(parity, host)] = (g, working)
 
-    def run(self, factors=None) -> DeviceFactorSet:
+    def _replay(self, host: bool):
         st = self.st
         if st.active_mode != 0:
             raise BufferOrderError(f"a sweep starts at mode 0, the tensor is at mode "
                                    f"{st.active_mode}")
+        key = (st.active, host)
+        if key not in self.graphs:
+            self._capture(host)
+        g, outs = self.graphs[key]
+        g.replay()
+        # host state of N swaps; the device counters were zeroed by the graph
+        st.active = st.active ^ (self.N % 2)
+        st._expected = self.N * st.nnz
+        check_errors(st)  # synchronizes: the host outputs are complete too
+        return outs
+
+    def run_host(self):
+        """Replay with the bound pinned buffers: host_in -> sweep -> host_out."""
+        if not hasattr(self, "host_in"):
+            raise RuntimeError("bind_host first")
+        self._replay(True)
+        return self.host_out
+
+    def run(self, factors=None) -> DeviceFactorSet:
+        st = self.st
         if factors is not None:
             fs = _coerce_factors(factors, st.device)
             fs.require_match(st.params.dims)
             for dst, src in zip(self.inputs, fs.factors):
                 if src.data_ptr() != dst.data_ptr():
                     dst.copy_(src, non_blocking=True)
-        if st.active not in self.graphs:
-            self._capture()
-        g, outs = self.graphs[st.active]
-        g.replay()
-        # host state of N swaps; the device counters were zeroed by the graph
-        st.active = st.active ^ (self.N % 2)
-        st._expected = self.N * st.nnz
-        check_errors(st)
+        outs = self._replay(False)
         return DeviceFactorSet(tuple(outs), self.lambdas, st.device, validate=False)

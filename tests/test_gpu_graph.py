@@ -58,3 +58,27 @@ def test_graph_replay_chained_inputs_and_errors():
     st.slot_maps[1][7] = -1
     with pytest.raises(ShardOverflowError):
         g.run()
+
+
+def test_graph_host_io_matches_eager():
+    """run_host: pinned inputs -> sweep -> pinned outputs, copies in the graph."""
+    from paper_2309_09131_b200 import DeviceFactorSet, sweep_all_modes
+    from paper_2309_09131_b200.graph import SweepGraph
+    dims, st, ref, smap = _case(3, 100_000)
+    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    g = SweepGraph(st, f0, smap)
+    for _ in range(2):
+        sweep_all_modes(ref, f0, smap)
+    host_in = [f.cpu().pin_memory() for f in f0.factors]
+    host_out = [torch.empty(f.shape, dtype=torch.float32).pin_memory() for f in f0.factors]
+    g.bind_host(host_in, host_out)
+    for rep in range(3):
+        fs = DeviceFactorSet.random(dims, 32, seed=20 + rep)
+        for h, f in zip(host_in, fs.factors):
+            h.copy_(f.cpu())
+        outs = g.run_host()
+        want = sweep_all_modes(ref, fs, smap)
+        for a, b in zip(outs, want.factors):
+            assert torch.equal(a, b.cpu()), rep
+    assert g.host_bytes() == (sum(f.numel() * 4 for f in f0.factors[1:]),
+                              sum(f.numel() * 4 for f in f0.factors))
