@@ -48,6 +48,47 @@ struct ModeArgs {
   PeerTable peers;
 };
 
+// Packed fp32 pairs: sm_100's FMUL2 / FFMA2 / FADD2 do two fp32 lanes per
+// instruction, each rounded exactly like the scalar op (bitwise-identical
+// sums, half the instructions).  A scalar operand packed as (v, v) becomes a
+// broadcast operand (no move).
+typedef unsigned long long f32x2;
+struct f32x4p {
+  f32x2 lo, hi;
+};
+__device__ __forceinline__ f32x2 f2_pack(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f32x2 r, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2_add(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x4p f4p(const float4 &x) {
+  return {f2_pack(x.x, x.y), f2_pack(x.z, x.w)};
+}
+__device__ __forceinline__ float4 f4u(const f32x4p &x) {
+  float4 r;
+  f2_unpack(x.lo, r.x, r.y);
+  f2_unpack(x.hi, r.z, r.w);
+  return r;
+}
+
 // Remap store of one record (CW4 16-byte words + optional separate value)
 // to slot s: this GPU's back buffer, or the owning peer's.  Out-of-range
 // slots raise FC_FLAG_SLOT_RANGE.

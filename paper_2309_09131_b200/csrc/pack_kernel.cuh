@@ -211,25 +211,24 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       int cur = s_piece_bin[gi];
       int nxt = cur + 1 < rows ? bin_start(cur + 1) : nvalid;
       bool head = pb > bin_start(cur);
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      // 4 columns as two packed fp32 pairs (FMUL2 / FFMA2)
+      f32x4p acc = {0ull, 0ull};
+      auto put = [](float *p, const f32x4p &x) { *reinterpret_cast<float4 *>(p) = f4u(x); };
       auto flush = [&]() {
         if (head) {
           if (lg == 0) s_bnd_row[2 * gi] = cur;
-          if (col_ok) VecT<4>::store(s_bnd + (2 * gi) * R + col, acc);
+          if (col_ok) put(s_bnd + (2 * gi) * R + col, acc);
         } else if (col_ok) {
           if (direct) {
-            VecT<4>::store(out_rows + cur * R + col, acc);
+            put(out_rows + cur * R + col, acc);
             return;
           }
           float *p = s_acc + cur * R + col;
-          float o[4];
-          VecT<4>::load(p, o);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) o[v] += acc[v];
-          VecT<4>::store(p, o);
+          const f32x4p o = f4p(*reinterpret_cast<const float4 *>(p));
+          put(p, {f2_add(o.lo, acc.lo), f2_add(o.hi, acc.hi)});
         }
       };
-      auto consume = [&](int p, float v, const float (&pr)[4]) {
+      auto consume = [&](int p, float v, const f32x4p &pr) {
         if (p == nxt) {  // a new row starts here
           flush();
           head = false;
@@ -237,25 +236,23 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
             ++cur;
             nxt = cur + 1 < rows ? bin_start(cur + 1) : nvalid;
           } while (nxt == p);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] = 0.f;
+          acc = {0ull, 0ull};
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] = fmaf(v, pr[k], acc[k]);
+        const f32x2 vv = f2_pack(v, v);
+        acc.lo = f2_fma(vv, pr.lo, acc.lo);
+        acc.hi = f2_fma(vv, pr.hi, acc.hi);
       };
       // column-offset factor bases, hoisted (the loop rematerialised them
       // from the parameter bank every iteration: 4.84 -> 4.69 ms on c2)
       const float *f1b = a.fac[W1] + col;
       const float *f2b = a.fac[W2] + col;
       const uint32_t rstride = (uint32_t)(RT > 0 ? RT : R);
-      auto prod = [&](uint32_t pk, float (&pr)[4]) {
+      auto prod = [&](uint32_t pk, f32x4p &pr) {
         const uint32_t c1 = pk >> shift, c2 = pk & lowmask;
-        const float4 f1 = __ldg(reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride));
-        const float4 f2 = __ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride));
-        pr[0] = f1.x * f2.x;
-        pr[1] = f1.y * f2.y;
-        pr[2] = f1.z * f2.z;
-        pr[3] = f1.w * f2.w;
+        const f32x4p f1 = f4p(__ldg(reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride)));
+        const f32x4p f2 = f4p(__ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride)));
+        pr.lo = f2_mul(f1.lo, f2.lo);
+        pr.hi = f2_mul(f1.hi, f2.hi);
       };
       const uint2 *sp = s_sorted + gi;  // pad of piece gi
       int p = pb;
@@ -263,7 +260,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         uint2 q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) q[u] = sp[p + u];
-        float pr[U][4];
+        f32x4p pr[U];
         if (col_ok) {
 #pragma unroll
           for (int u = 0; u < U; ++u) prod(q[u].x, pr[u]);
@@ -273,14 +270,14 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
       for (; p < pe; ++p) {
         const uint2 q = sp[p];
-        float pr[4];
+        f32x4p pr;
         if (col_ok) prod(q.x, pr);
         consume(p, __uint_as_float(q.y), pr);
       }
       const bool tail = pe < nvalid && nxt > pe;
       if (tail && !head) {
         if (lg == 0) s_bnd_row[2 * gi + 1] = cur;
-        if (col_ok) VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, acc);
+        if (col_ok) put(s_bnd + (2 * gi + 1) * R + col, acc);
       } else {
         flush();
       }
