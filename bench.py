@@ -426,7 +426,9 @@ def run_ours(args, rank, world, local):
                         "all_gather_into_tensor of updated factor rows"),
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
-                       "mode_ms": [round(1e3 * x, 4) for x in mode_secs[:N]]},
+                       # median over the measured sweeps of each mode pass
+                       "mode_ms": [round(1e3 * statistics.median(mode_secs[n::N]), 4)
+                                   for n in range(N)] if mode_secs else []},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name(N, dims, R) + " (+ reduce_level_kernel)",
