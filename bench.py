@@ -385,7 +385,11 @@ def run_ours(args, rank, world, local):
 
             h2d = sum(h.numel() * 4 for h in host_in)
             d2h = sum(h.numel() * 4 for h in host_out) if updated else sum(d * R * 4 for d in dims)
-            path = "sweep_all_modes(DeviceShardedTensor, factors<-pinned host) -> pinned host"
+            path = ("peer_sweep_all_modes(PeerShardedTensor, factors<-pinned host) -> pinned host"
+                    if dt is not None and exchange == "p2p" else
+                    "dist_sweep_all_modes(DistShardedTensor, factors<-pinned host) -> pinned host"
+                    if dt is not None else
+                    "sweep_all_modes(DeviceShardedTensor, factors<-pinned host) -> pinned host")
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()

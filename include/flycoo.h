@@ -141,6 +141,12 @@ int fc_ipc_handle(const void *ptr, void *handle);
 int fc_ipc_open(const void *handle, void **ptr);
 int fc_ipc_close(void *ptr);
 int fc_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
+/* Cross-GPU ordering on the stream, without the host: the GPU's front end
+ * writes `value` to a (peer-mapped) 32-bit flag after fencing the stream's
+ * prior memory operations, or waits until (int32)(*flag - value) >= 0
+ * (cuStreamWriteValue32 / cuStreamWaitValue32; no SM spins). */
+int fc_stream_signal(void *flag, uint32_t value, void *stream);
+int fc_stream_wait(const void *flag, uint32_t value, void *stream);
 
 /* Cursor remap strategy (_kernels.py:73-80): b = src_sid[i, next_mode];
  * slot = dest_base[b] + fetch_add(cursors[b]); dst[slot] = src[i] together

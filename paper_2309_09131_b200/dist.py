@@ -194,8 +194,10 @@ class DistShardedTensor:
         if key not in self._work:
             lp = _local_plan(self.plan, mode, self.plans[mode])
             # same chunking as the single-GPU plan -> bitwise-identical sums
+            p = self.plans[mode]
             self._work[key] = make_mode_work(lp, mode, rank_r, self.device,
-                                             chunk_elems=default_chunk_elems(self.plan.nnz))
+                                             chunk_elems=default_chunk_elems(self.plan.nnz),
+                                             ss_range=(p.ss_lo, p.ss_hi))
         return self._work[key]
 
     def owned_rows(self, mode: int):

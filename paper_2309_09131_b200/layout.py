@@ -188,20 +188,24 @@ def direct_groups(counts: np.ndarray, tile: int, group: int):
 
 
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None,
-                   merge: bool = True) -> ModeWork:
+                   merge: bool = True, ss_range: tuple | None = None) -> ModeWork:
     """Split every super-shard of `mode` into CTA chunks.  Shared-memory
     accumulation (m rows fit): chunks of `chunk_elems`, super-shards with
     several chunks get one partial tile per chunk, summed in chunk order by
     K2; on the fast path consecutive small super-shards are merged into one
     chunk (rows <= fc_chunk_rows_max).  Otherwise one chunk per super-shard
-    accumulating in `out`."""
+    accumulating in `out`.  `ss_range` = (lo, hi) restricts the work to those
+    super-shards (a GPU's owned range in the multi-GPU sweep): no chunks or
+    zeroing tasks for the rows other GPUs own."""
     L = _lib.load()
     params = plan.params
     m = int(params.m[mode])
     counts = np.asarray(plan.ss_counts[mode], dtype=np.int64)
     offs = np.asarray(plan.ss_elem_offsets[mode], dtype=np.int64)
+    lo, hi = (0, counts.shape[0]) if ss_range is None else (int(ss_range[0]), int(ss_range[1]))
+    counts, offs = counts[lo:hi], offs[lo:hi + 1]
     k = counts.shape[0]
-    nnz = plan.nnz
+    nnz = int(offs[-1]) if ss_range is not None else plan.nnz  # end of the last chunk
     tile = int(L.fc_tile_elems())
     smem = m <= int(L.fc_smem_acc_rows_max(int(rank)))
     dev = torch.device(device)
@@ -224,7 +228,7 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
         starts = offs[ss_of] + j * C
         chunk_start = np.concatenate((starts, [nnz])).astype(np.int64)
         rows = np.minimum(np.where(big[grp_of], 1, nss[grp_of]) * m,
-                          params.dims[mode] - ss_of * m).astype(np.int32)
+                          params.dims[mode] - (ss_of + lo) * m).astype(np.int32)
         nch_ss = np.ones(k, dtype=np.int64)
         nch_ss[first[big]] = pieces[big]
         multi = nch_ss >= 2
@@ -234,10 +238,12 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
                         PART_DIRECT).astype(np.int32)
         nparts = int(part_base[-1])
         r1, r2, nslots = reduce_plan(nch_ss, part_base)
+        r1[:, 0] += lo
+        r2[:, 0] += lo
         ws = (torch.empty(max(nparts * m * rank, 1), dtype=torch.float32, device=dev)
               if nparts or r1.shape[0] else None)
         ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
-        return ModeWork(True, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), t(rows),
+        return ModeWork(True, total, t(chunk_start), t((ss_of + lo).astype(np.int32)), t(part), t(rows),
                         m, int(rows.max()) if rows.size else m, t(r1), int(r1.shape[0]), t(r2),
                         int(r2.shape[0]), nparts, ws, ws2, C)
     if smem:
@@ -260,6 +266,8 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
         part = np.where(multi[ss_of], part_base[:-1][ss_of] + j, -1).astype(np.int32)
         nparts = int(part_base[-1])
         r1, r2, nslots = reduce_plan(nch, part_base)
+        r1[:, 0] += lo
+        r2[:, 0] += lo
     else:
         part = np.full(total, -1, dtype=np.int32)
         nparts, nslots = 0, 0
@@ -270,7 +278,7 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
     ws = (torch.empty(max(nparts * m * rank, 1), dtype=torch.float32, device=dev)
           if nparts or r1.shape[0] else None)
     ws2 = torch.empty(nslots * m * rank, dtype=torch.float32, device=dev) if nslots else None
-    return ModeWork(smem, total, t(chunk_start), t(ss_of.astype(np.int32)), t(part), None, m, m,
+    return ModeWork(smem, total, t(chunk_start), t((ss_of + lo).astype(np.int32)), t(part), None, m, m,
                     t(r1), int(r1.shape[0]), t(r2), int(r2.shape[0]), nparts, ws, ws2, C)
 
 

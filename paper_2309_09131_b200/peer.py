@@ -15,9 +15,12 @@ single-GPU mode-n buffer -- but no send region, all-to-all or unpack pass:
   factor from their output buffers (copy engines over NVLink) -- the
   all-gather of engine.sweep_all_modes' factor replacement (engine.py:292).
 
-The barrier between modes (stream synchronize + ``dist.barrier``) orders
-"all peers finished writing my back buffer / reading their front buffer"
-before the swap; kernels never wait on other GPUs.  After every mode each
+Between modes the GPUs order themselves on the device: each signals an
+epoch flag in every peer's memory with a stream write (fenced after its
+pass) and waits for all peers' flags with stream waits -- "all peers
+finished writing my back buffer / reading their front buffer" -- without a
+host round trip or any SM spinning (``FLYCOO_PEER_SYNC=host``: stream
+synchronize + ``dist.barrier``).  After every mode each
 GPU's slice equals the single-GPU buffer's slice bit-exactly
 (tests/test_gpu_peer.py).
 """
@@ -25,6 +28,7 @@ GPU's slice equals the single-GPU buffer's slice bit-exactly
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -148,6 +152,13 @@ class PeerShardedTensor:
         self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._expected = 0
         self._opened = []
+        # cross-GPU ordering between passes: flags[q] = last epoch GPU q
+        # signalled to this GPU (stream memory operations, no host round trip);
+        # FLYCOO_PEER_SYNC=host falls back to stream synchronize + dist.barrier
+        self.flags = self._alloc((world,), torch.int32)
+        self.peer_flags = None
+        self.epoch = 0
+        self.device_sync = ipc and os.environ.get("FLYCOO_PEER_SYNC", "device") != "host"
 
     # -- buffers and peer wiring
     def _alloc(self, shape, dtype):
@@ -181,10 +192,12 @@ class PeerShardedTensor:
         return out
 
     def connect(self):
-        """Collective over the group: map every peer's record buffers."""
-        ptrs = self._exchange_ptrs(self._shared())
+        """Collective over the group: map every peer's record buffers and
+        barrier flags."""
+        ptrs = self._exchange_ptrs(self._shared() + [self.flags])
         self.peer_crd = [ptrs[0], ptrs[1]]
         self.peer_val = None if self.val[0] is None else [ptrs[2], ptrs[3]]
+        self.peer_flags = ptrs[-1]
 
     @staticmethod
     def connect_local(ranks):
@@ -220,8 +233,10 @@ class PeerShardedTensor:
         key = (mode, R)
         if key not in self._work:
             lp = _local_plan(self.plan, mode, self.plans[mode])
+            p = self.plans[mode]
             self._work[key] = make_mode_work(lp, mode, R, self.device,
-                                             chunk_elems=default_chunk_elems(self.plan.nnz))
+                                             chunk_elems=default_chunk_elems(self.plan.nnz),
+                                             ss_range=(p.ss_lo, p.ss_hi))
         return self._work[key]
 
     def owned_rows(self, mode: int):
@@ -290,9 +305,28 @@ class PeerShardedTensor:
                                f"flags {flags:#x}")
 
     def barrier(self):
+        """Host barrier: every GPU's queued work done (stream synchronize),
+        then dist.barrier."""
         torch.cuda.current_stream().synchronize()
         if self.ipc:
             dist.barrier(group=self.group)
+
+    def sync(self):
+        """Order the GPUs between passes: after it, every peer's previous pass
+        (records stored into this GPU, owned output rows) is complete and
+        visible, and no peer still reads this GPU's front buffer."""
+        if not self.device_sync:
+            self.barrier()
+            return
+        self.epoch += 1
+        st = torch.cuda.current_stream().cuda_stream
+        for q in range(self.world):
+            if q != self.rank:
+                _lib.call("fc_stream_signal", self.peer_flags[q] + 4 * self.rank, self.epoch, st)
+        base = self.flags.data_ptr()
+        for q in range(self.world):
+            if q != self.rank:
+                _lib.call("fc_stream_wait", base + 4 * q, self.epoch, st)
 
     def close(self):
         for ptr in self._opened:
@@ -312,7 +346,7 @@ def peer_mttkrp_mode(dt: PeerShardedTensor, factors, mode: int) -> torch.Tensor:
     R = int(factors[0].shape[1])
     out, ptrs = dt.output(mode, R)
     dt.mode_pass(factors, mode, out)
-    dt.barrier()
+    dt.sync()
     dt.pull_rows(mode, out, ptrs)
     dt.swap()
     return out
@@ -323,6 +357,7 @@ def peer_sweep_all_modes(dt: PeerShardedTensor, factors, mode_seconds=None):
     returned factors are the persistent output buffers (valid until the
     next sweep on `dt` rewrites them)."""
     working = list(factors)
+    events = []
     for n in range(dt.num_modes):
         if mode_seconds is not None:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -331,7 +366,8 @@ def peer_sweep_all_modes(dt: PeerShardedTensor, factors, mode_seconds=None):
         if mode_seconds is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
-            e1.synchronize()
-            mode_seconds.append(e0.elapsed_time(e1) / 1e3)
-    dt.check()
+            events.append((e0, e1))
+    dt.check()  # synchronizes this GPU's stream
+    if mode_seconds is not None:
+        mode_seconds.extend(a.elapsed_time(b) / 1e3 for a, b in events)
     return working

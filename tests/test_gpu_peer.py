@@ -97,7 +97,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, result):
+def _ipc_worker(rank, world, port, result, sync):
+    os.environ["FLYCOO_PEER_SYNC"] = sync
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -111,15 +112,18 @@ def _ipc_worker(rank, world, port, result):
             ref = build(coords, vals, params)
             dt = PeerShardedTensor(st, world, rank)
             dt.connect()
+            assert dt.device_sync == (sync == "device")
             f0 = DeviceFactorSet.random(dims, 32, seed=3)
-            got = peer_sweep_all_modes(dt, list(f0.factors))
             ref_working = list(f0.factors)
+            got = list(f0.factors)
             smap = schedule_super_shards(ref.plan, 1)
-            for n in range(N):
-                ref_working[n] = mttkrp_mode(ref, DeviceFactorSet(ref_working, None, validate=False),
-                                             n, smap)
-            for n in range(N):
-                assert torch.allclose(got[n], ref_working[n], rtol=1e-5, atol=0), (rank, N, n)
+            for sweep in range(3):  # chained sweeps: outputs feed the next sweep
+                got = [g.clone() for g in peer_sweep_all_modes(dt, got)]
+                for n in range(N):
+                    ref_working[n] = mttkrp_mode(
+                        ref, DeviceFactorSet(ref_working, None, validate=False), n, smap)
+                for n in range(N):
+                    assert torch.allclose(got[n], ref_working[n], rtol=1e-5, atol=0), (rank, N, n)
             p = dt.plans[0]
             c, v = dt.local_records()
             assert torch.equal(c, ref.crd[ref.active][p.e_lo:p.e_hi]), (rank, N)
@@ -131,9 +135,10 @@ def _ipc_worker(rank, world, port, result):
         dist.destroy_process_group()
 
 
-def test_peer_exchange_two_processes_ipc():
+@pytest.mark.parametrize("sync", ["device", "host"])
+def test_peer_exchange_two_processes_ipc(sync):
     ctx = mp.get_context("spawn")
     result = ctx.Manager().dict()
-    mp.start_processes(_ipc_worker, args=(2, _free_port(), result), nprocs=2, join=True,
+    mp.start_processes(_ipc_worker, args=(2, _free_port(), result, sync), nprocs=2, join=True,
                        start_method="spawn")
     assert sorted(result.keys()) == [0, 1]
