@@ -141,6 +141,11 @@ int fc_ipc_handle(const void *ptr, void *handle);
 int fc_ipc_open(const void *handle, void **ptr);
 int fc_ipc_close(void *ptr);
 int fc_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
+/* Factor-row all-gather of the fused exchange in one launch: rows
+ * [row_lo[q], row_lo[q+1]) of peer_src[q] (GPU q's output, peer-mapped) are
+ * copied into dst for every q != self; rows are row_floats fp32 wide. */
+int fc_gather_peer_rows(float *dst, const float *const *peer_src, const int64_t *row_lo,
+                        int npeers, int self, int64_t row_floats, void *stream);
 /* Cross-GPU ordering on the stream, without the host: the GPU's front end
  * writes `value` to a (peer-mapped) 32-bit flag after fencing the stream's
  * prior memory operations, or waits until (int32)(*flag - value) >= 0

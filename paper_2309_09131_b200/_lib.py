@@ -61,6 +61,7 @@ _SIGS = {
     "fc_ipc_open": (_int, [_vp, _vp]),
     "fc_ipc_close": (_int, [_vp]),
     "fc_copy_async": (_int, [_vp, _vp, _i64, _vp]),
+    "fc_gather_peer_rows": (_int, [_vp, _vp, _vp, _int, _int, _i64, _vp]),
     "fc_stream_signal": (_int, [_vp, _c.c_uint32, _vp]),
     "fc_stream_wait": (_int, [_vp, _c.c_uint32, _vp]),
     "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),

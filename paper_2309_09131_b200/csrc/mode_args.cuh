@@ -22,6 +22,13 @@ struct PeerTable {
   int64_t base[kMaxPeers + 1];
 };
 
+// Owned output-row ranges of the GPUs (factor-row all-gather).
+struct PeerRows {
+  int n;
+  const float *src[kMaxPeers];
+  int64_t row_lo[kMaxPeers + 1];
+};
+
 struct ModeArgs {
   const int4 *src;
   const float *src_val;

@@ -8,10 +8,27 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "mode_args.cuh"
 
 using namespace fc;
 
 namespace {
+// One launch for the factor-row all-gather of the fused exchange: GPU q's
+// owned rows [row_lo[q], row_lo[q+1]) are read from q's output buffer over
+// NVLink (16-B loads) into this GPU's copy.  Blocks stride over the rows of
+// all peers; the local range (self) is skipped.
+__global__ void __launch_bounds__(256) gather_peer_rows_kernel(float4 *dst, PeerRows pr, int self,
+                                                               int64_t row_vec) {
+  for (int q = 0; q < pr.n; ++q) {
+    if (q == self) continue;
+    const float4 *src = reinterpret_cast<const float4 *>(pr.src[q]);
+    const int64_t v0 = pr.row_lo[q] * row_vec, v1 = pr.row_lo[q + 1] * row_vec;
+    for (int64_t v = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
+         v += (int64_t)gridDim.x * blockDim.x)
+      dst[v] = src[v];
+  }
+}
+
 // Stream memory operations, resolved through the runtime so the library has
 // no link-time dependency on libcuda (it loads on hosts without a driver).
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -68,6 +85,30 @@ int fc_copy_async(void *dst, const void *src, int64_t bytes, void *stream) {
   FC_CHECK_ARG(bytes >= 0 && (bytes == 0 || (dst && src)), "bad copy");
   if (bytes == 0) return FC_OK;
   FC_CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, as_stream(stream)));
+  return FC_OK;
+}
+
+int fc_gather_peer_rows(float *dst, const float *const *peer_src, const int64_t *row_lo,
+                        int npeers, int self, int64_t row_floats, void *stream) {
+  FC_CHECK_ARG(npeers >= 1 && npeers <= kMaxPeers, "npeers %d outside [1, %d]", npeers, kMaxPeers);
+  FC_CHECK_ARG(dst && peer_src && row_lo, "null argument");
+  FC_CHECK_ARG(row_floats > 0 && row_floats % 4 == 0, "row width must be a multiple of 4 floats");
+  PeerRows pr{};
+  pr.n = npeers;
+  int64_t vecs = 0;
+  for (int q = 0; q < npeers; ++q) {
+    FC_CHECK_ARG(q == self || peer_src[q], "null peer rows %d", q);
+    FC_CHECK_ARG(row_lo[q + 1] >= row_lo[q], "row ranges not monotone");
+    pr.src[q] = peer_src[q];
+    pr.row_lo[q] = row_lo[q];
+    if (q != self) vecs += (row_lo[q + 1] - row_lo[q]) * (row_floats / 4);
+  }
+  pr.row_lo[npeers] = row_lo[npeers];
+  if (vecs == 0) return FC_OK;
+  const int grid = (int)min64((vecs + 255) / 256, 148 * 8);
+  gather_peer_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<float4 *>(dst), pr,
+                                                             self, row_floats / 4);
+  FC_LAUNCH_CHECK();
   return FC_OK;
 }
 

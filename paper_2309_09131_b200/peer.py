@@ -281,9 +281,15 @@ class PeerShardedTensor:
         """Copy the peers' owned rows of `mode` into `out` (NVLink copy
         engines); `out` then holds the whole updated factor."""
         R = int(out.shape[1])
-        row_bytes = R * 4
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-        for q, (lo, hi) in enumerate(self.row_ranges(mode)):
+        ranges = self.row_ranges(mode)
+        bounds = [lo for lo, _ in ranges] + [ranges[-1][1]]
+        if R % 4 == 0:  # one launch, NVLink loads
+            _lib.call("fc_gather_peer_rows", out.data_ptr(), _lib.ptr_array(peer_out_ptrs),
+                      _lib.i64_array(bounds), self.world, self.rank, R, st)
+            return
+        row_bytes = R * 4
+        for q, (lo, hi) in enumerate(ranges):
             if q == self.rank or hi <= lo:
                 continue
             off = lo * row_bytes
