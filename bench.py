@@ -275,15 +275,22 @@ def run_ours(args, rank, world, local):
     # single GPU, updated semantics: the sweep is replayed as a CUDA graph
     # (graph.py; FLYCOO_GRAPH=0 for eager launches).  Per-mode times come from
     # eager sweeps (the replay is one launch).
-    graph = None
-    if dt is None and updated and os.environ.get("FLYCOO_GRAPH", "1") != "0":
+    graph = peer_graph = None
+    use_graph = updated and os.environ.get("FLYCOO_GRAPH", "1") != "0"
+    if dt is None and use_graph:
         from paper_2309_09131_b200.graph import SweepGraph
         graph = SweepGraph(st, factors, smap)
+    elif use_graph and exchange == "p2p" and dt.device_sync:
+        # multi-GPU: the sweep with its device-side barriers as one graph per GPU
+        from paper_2309_09131_b200.peer import PeerSweepGraph
+        peer_graph = PeerSweepGraph(dt, list(factors.factors))
 
     def step(fs, mode_secs=None, eager=False):
         flist = fs.factors if hasattr(fs, "factors") else fs
         if graph is not None and not eager:
             return graph.run(fs).factors
+        if peer_graph is not None and not eager:
+            return peer_graph.run(list(flist))
         if dt is not None and exchange == "p2p":
             if updated:
                 return peer_sweep_all_modes(dt, list(flist), mode_seconds=mode_secs)
@@ -335,7 +342,7 @@ def run_ours(args, rank, world, local):
     ms_per_step = t_ms / args.steps
     # strong scaling for world > 1: the ranks share one tensor
     value = N * nnz / (ms_per_step / 1e3)
-    if graph is not None:  # per-mode pass times from eager sweeps
+    if graph is not None or peer_graph is not None:  # per-mode times from eager sweeps
         for _ in range(args.steps):
             step(factors, mode_secs, eager=True)
 
@@ -347,8 +354,9 @@ def run_ours(args, rank, world, local):
     achieved = sum(per_mode) / world * args.steps / kern_s / 1e9
     peak, peak_src = peaks()
     src = dt if dt is not None else st
-    launches_per_step = sum(src.mode_work(n, R).launches +
-                            (1 if dt is not None and exchange != "p2p" else 0) for n in range(N))
+    # + the unpack (NCCL exchange) or the row gather (fused exchange) per mode
+    launches_per_step = sum(src.mode_work(n, R).launches + (1 if dt is not None else 0)
+                            for n in range(N))
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
@@ -385,7 +393,9 @@ def run_ours(args, rank, world, local):
 
             h2d = sum(h.numel() * 4 for h in host_in)
             d2h = sum(h.numel() * 4 for h in host_out) if updated else sum(d * R * 4 for d in dims)
-            path = ("peer_sweep_all_modes(PeerShardedTensor, factors<-pinned host) -> pinned host"
+            path = ("PeerSweepGraph(PeerShardedTensor).run(factors<-pinned host) -> pinned host"
+                    if peer_graph is not None else
+                    "peer_sweep_all_modes(PeerShardedTensor, factors<-pinned host) -> pinned host"
                     if dt is not None and exchange == "p2p" else
                     "dist_sweep_all_modes(DistShardedTensor, factors<-pinned host) -> pinned host"
                     if dt is not None else

@@ -15,9 +15,9 @@ single-GPU mode-n buffer -- but no send region, all-to-all or unpack pass:
   factor from their output buffers (copy engines over NVLink) -- the
   all-gather of engine.sweep_all_modes' factor replacement (engine.py:292).
 
-Between modes the GPUs order themselves on the device: each signals an
-epoch flag in every peer's memory with a stream write (fenced after its
-pass) and waits for all peers' flags with stream waits -- "all peers
+Between modes the GPUs order themselves on the device: each sets a
+per-mode flag in every peer's memory with a stream write (fenced after its
+pass), waits for all peers' flags with stream waits and resets them -- "all peers
 finished writing my back buffer / reading their front buffer" -- without a
 host round trip or any SM spinning (``FLYCOO_PEER_SYNC=host``: stream
 synchronize + ``dist.barrier``).  After every mode each
@@ -40,7 +40,7 @@ from .dist import _local_plan, partition_super_shards
 from .layout import DeviceShardedTensor, PartitionPlan, default_chunk_elems, make_mode_work
 
 __all__ = ["PeerModePlan", "peer_plans", "IpcBuffer", "PeerShardedTensor", "peer_mttkrp_mode",
-           "peer_sweep_all_modes"]
+           "peer_sweep_all_modes", "PeerSweepGraph"]
 
 
 @dataclass
@@ -152,12 +152,15 @@ class PeerShardedTensor:
         self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._expected = 0
         self._opened = []
-        # cross-GPU ordering between passes: flags[q] = last epoch GPU q
-        # signalled to this GPU (stream memory operations, no host round trip);
-        # FLYCOO_PEER_SYNC=host falls back to stream synchronize + dist.barrier
-        self.flags = self._alloc((world,), torch.int32)
+        # cross-GPU ordering between passes (stream memory operations, no host
+        # round trip): flags[n][q] = 1 once GPU q finished its mode-n pass;
+        # reset to 0 by this GPU after its wait.  Constant values make the
+        # protocol replayable in a CUDA graph; a peer's next signal on the same
+        # slot always follows this GPU's reset (it first waits on a later
+        # mode's signal of ours).  FLYCOO_PEER_SYNC=host: stream synchronize +
+        # dist.barrier instead.
+        self.flags = self._alloc((self.num_modes, world), torch.int32)
         self.peer_flags = None
-        self.epoch = 0
         self.device_sync = ipc and os.environ.get("FLYCOO_PEER_SYNC", "device") != "host"
 
     # -- buffers and peer wiring
@@ -317,22 +320,23 @@ class PeerShardedTensor:
         if self.ipc:
             dist.barrier(group=self.group)
 
-    def sync(self):
-        """Order the GPUs between passes: after it, every peer's previous pass
-        (records stored into this GPU, owned output rows) is complete and
-        visible, and no peer still reads this GPU's front buffer."""
+    def sync(self, mode: int = 0):
+        """Order the GPUs after the mode-`mode` pass: afterwards every peer's
+        pass (records stored into this GPU, owned output rows) is complete
+        and visible, and no peer still reads this GPU's front buffer."""
         if not self.device_sync:
             self.barrier()
             return
-        self.epoch += 1
         st = torch.cuda.current_stream().cuda_stream
+        slot = 4 * mode * self.world
         for q in range(self.world):
             if q != self.rank:
-                _lib.call("fc_stream_signal", self.peer_flags[q] + 4 * self.rank, self.epoch, st)
-        base = self.flags.data_ptr()
+                _lib.call("fc_stream_signal", self.peer_flags[q] + slot + 4 * self.rank, 1, st)
+        base = self.flags.data_ptr() + slot
         for q in range(self.world):
             if q != self.rank:
-                _lib.call("fc_stream_wait", base + 4 * q, self.epoch, st)
+                _lib.call("fc_stream_wait", base + 4 * q, 1, st)
+                _lib.call("fc_stream_signal", base + 4 * q, 0, st)
 
     def close(self):
         for ptr in self._opened:
@@ -352,7 +356,7 @@ def peer_mttkrp_mode(dt: PeerShardedTensor, factors, mode: int) -> torch.Tensor:
     R = int(factors[0].shape[1])
     out, ptrs = dt.output(mode, R)
     dt.mode_pass(factors, mode, out)
-    dt.sync()
+    dt.sync(mode)
     dt.pull_rows(mode, out, ptrs)
     dt.swap()
     return out
@@ -377,3 +381,66 @@ def peer_sweep_all_modes(dt: PeerShardedTensor, factors, mode_seconds=None):
     if mode_seconds is not None:
         mode_seconds.extend(a.elapsed_time(b) / 1e3 for a, b in events)
     return working
+
+
+class PeerSweepGraph:
+    """CUDA-graph replay of :func:`peer_sweep_all_modes` on this GPU: the
+    mode passes, the device-side barriers (stream memory operations with
+    constant flag values, hence replayable) and the row gathers of a whole
+    sweep in one launch -- no host work between modes.  Every GPU of the
+    group builds and runs its own graph; outputs are the persistent
+    per-mode buffers (valid until the next run)."""
+
+    def __init__(self, dt: PeerShardedTensor, factors):
+        if not dt.device_sync:
+            raise ValueError("graph replay needs the device-side barrier (FLYCOO_PEER_SYNC=device)")
+        if dt.active_mode != 0:
+            raise ValueError(f"a sweep starts at mode 0, the tensor is at mode {dt.active_mode}")
+        self.dt = dt
+        self.N = dt.num_modes
+        self.inputs = [f.clone() for f in factors]
+        self.R = int(self.inputs[0].shape[1])
+        self.pool = torch.cuda.graph_pool_handle()
+        self.graphs = {}
+        # eager sweeps: cache work plans, create and map the output buffers
+        # (collective), configure the kernels -- both buffer parities
+        for _ in range(1 if self.N % 2 == 0 else 2):
+            peer_sweep_all_modes(dt, list(self.inputs))
+        torch.cuda.synchronize()
+
+    def _capture(self):
+        dt = self.dt
+        saved = (dt.active, dt.active_mode, dt._expected)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dt.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, pool=self.pool, stream=side):
+                dt._stat.zero_()
+                working = list(self.inputs)
+                for n in range(self.N):
+                    out, ptrs = dt.output(n, self.R)
+                    dt.mode_pass(working, n, out)
+                    dt.sync(n)
+                    dt.pull_rows(n, out, ptrs)
+                    dt.swap()
+                    working[n] = out
+        torch.cuda.current_stream().wait_stream(side)
+        expected = dt._expected - saved[2]
+        dt.active, dt.active_mode, dt._expected = saved
+        self.graphs[saved[0]] = (g, working, expected)
+
+    def run(self, factors=None):
+        dt = self.dt
+        if factors is not None:
+            for dst, src in zip(self.inputs, factors):
+                if src.data_ptr() != dst.data_ptr():
+                    dst.copy_(src, non_blocking=True)
+        if dt.active not in self.graphs:
+            self._capture()
+        g, outs, expected = self.graphs[dt.active]
+        g.replay()
+        dt.active ^= self.N % 2
+        dt._expected = expected
+        dt.check()
+        return outs

@@ -127,6 +127,25 @@ def _ipc_worker(rank, world, port, result, sync):
             p = dt.plans[0]
             c, v = dt.local_records()
             assert torch.equal(c, ref.crd[ref.active][p.e_lo:p.e_hi]), (rank, N)
+            if sync == "device":  # the whole sweep as a CUDA graph, chained replays
+                from paper_2309_09131_b200.peer import PeerSweepGraph
+                g = PeerSweepGraph(dt, got)
+                for _ in range(1 if N % 2 == 0 else 2):  # the graph's warm-up sweeps
+                    for n in range(N):
+                        ref_working[n] = mttkrp_mode(
+                            ref, DeviceFactorSet(ref_working, None, validate=False), n, smap)
+                got = [t.clone() for t in ref_working]
+                for rep in range(3):
+                    got = [t.clone() for t in g.run(got)]
+                    for n in range(N):
+                        ref_working[n] = mttkrp_mode(
+                            ref, DeviceFactorSet(ref_working, None, validate=False), n, smap)
+                    for n in range(N):
+                        assert torch.allclose(got[n], ref_working[n], rtol=1e-5, atol=0), \
+                            ("graph", rank, N, rep, n)
+                p = dt.plans[0]
+                c, v = dt.local_records()
+                assert torch.equal(c, ref.crd[ref.active][p.e_lo:p.e_hi]), ("graph", rank, N)
             dt.barrier()
             dt.close()
             dist.barrier()
