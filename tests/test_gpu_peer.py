@@ -154,10 +154,10 @@ def _ipc_worker(rank, world, port, result, sync):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sync", ["device", "host"])
-def test_peer_exchange_two_processes_ipc(sync):
+@pytest.mark.parametrize("world,sync", [(2, "device"), (2, "host"), (3, "device")])
+def test_peer_exchange_processes_ipc(world, sync):
     ctx = mp.get_context("spawn")
     result = ctx.Manager().dict()
-    mp.start_processes(_ipc_worker, args=(2, _free_port(), result, sync), nprocs=2, join=True,
-                       start_method="spawn")
-    assert sorted(result.keys()) == [0, 1]
+    mp.start_processes(_ipc_worker, args=(world, _free_port(), result, sync), nprocs=world,
+                       join=True, start_method="spawn")
+    assert sorted(result.keys()) == list(range(world))
