@@ -37,7 +37,7 @@ class SweepGraph:
     updated factors -- tensors owned by the graph, overwritten by the next
     run (clone to keep them)."""
 
-    def __init__(self, st: DeviceShardedTensor, factors, smap):
+    def __init__(self, st: DeviceShardedTensor, factors, smap, updated: bool = True):
         if not st.canonical:
             raise BufferOrderError("graph replay needs the slot (canonical) layout")
         if st.active_mode != 0:
@@ -46,6 +46,10 @@ class SweepGraph:
         fs = _coerce_factors(factors, st.device)
         fs.require_match(st.params.dims)
         self.st, self.smap = st, smap
+        # updated: engine.sweep_all_modes (factor n replaced after mode n);
+        # fixed: every mode reads the input factors (the per-mode loop of
+        # BASELINE configs 1 and 3, bench.py:294-298 of the reference)
+        self.updated = updated
         self.rank = fs.rank
         self.lambdas = fs.lambdas.copy()
         self.inputs = [f.clone() for f in fs.factors]
@@ -61,8 +65,9 @@ class SweepGraph:
 
     def bind_host(self, host_in, host_out):
         """Pinned host buffers for :meth:`run_host`: `host_in[w]` feeds input
-        factor w (only w >= 1 is read: mode 0's output replaces factor 0
-        before anything reads it), `host_out[n]` receives updated factor n.
+        factor w (updated sweep: only w >= 1 is read -- mode 0's output
+        replaces factor 0 before anything reads it), `host_out[n]` receives
+        the output of mode n.
         The copies are part of the graph: each output's device-to-host copy
         runs on a side stream while the later modes compute."""
         for t in list(host_in) + list(host_out):
@@ -73,7 +78,8 @@ class SweepGraph:
 
     def host_bytes(self):
         """(h2d, d2h) bytes one run_host moves."""
-        return (sum(t.numel() * t.element_size() for t in self.host_in[1:]),
+        first = 1 if self.updated else 0
+        return (sum(t.numel() * t.element_size() for t in self.host_in[first:]),
                 sum(t.numel() * t.element_size() for t in self.host_out))
 
     def _capture(self, host: bool):
@@ -88,22 +94,25 @@ class SweepGraph:
             with torch.cuda.graph(g, pool=self.pool, stream=side):
                 st._stat.zero_()
                 if host:
-                    for w in range(1, self.N):
+                    for w in range(1 if self.updated else 0, self.N):
                         self.inputs[w].copy_(self.host_in[w], non_blocking=True)
                 working = list(self.inputs)
+                outs = []
                 for n in range(self.N):
                     cur = DeviceFactorSet(tuple(working), self.lambdas, st.device, validate=False)
-                    working[n] = mttkrp_mode(st, cur, n, self.smap, check=False)
+                    outs.append(mttkrp_mode(st, cur, n, self.smap, check=False))
+                    if self.updated:
+                        working[n] = outs[n]
                     if host:  # fork: copy out mode n while the next modes run
                         copies.wait_stream(side)
                         with torch.cuda.stream(copies):
-                            self.host_out[n].copy_(working[n], non_blocking=True)
+                            self.host_out[n].copy_(outs[n], non_blocking=True)
                 if host:
                     side.wait_stream(copies)  # join
         torch.cuda.current_stream().wait_stream(side)
         # capture ran the host side once: restore the tensor's host state
         st.active, st.active_mode, st._expected = saved
-        self.graphs[(parity, host)] = (g, working)
+        self.graphs[(parity, host)] = (g, outs)
 
     def _replay(self, host: bool):
         st = self.st

@@ -82,3 +82,19 @@ def test_graph_host_io_matches_eager():
             assert torch.equal(a, b.cpu()), rep
     assert g.host_bytes() == (sum(f.numel() * 4 for f in f0.factors[1:]),
                               sum(f.numel() * 4 for f in f0.factors))
+
+
+def test_graph_fixed_factor_loop_matches_eager():
+    """updated=False: every mode reads the input factors (configs 1 and 3)."""
+    from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, sweep_all_modes
+    from paper_2309_09131_b200.graph import SweepGraph
+    dims, st, ref, smap = _case(4, 100_000)
+    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    g = SweepGraph(st, f0, smap, updated=False)
+    sweep_all_modes(ref, f0, smap)  # N = 4: one warm-up sweep
+    for rep in range(3):
+        fs = DeviceFactorSet.random(dims, 32, seed=30 + rep)
+        got = g.run(fs)
+        want = [mttkrp_mode(ref, fs, n, smap) for n in range(4)]
+        for a, b in zip(got.factors, want):
+            assert torch.equal(a, b), rep
