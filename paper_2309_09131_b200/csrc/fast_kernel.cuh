@@ -5,7 +5,8 @@
 // N <= 4 (one 16-B coordinate word per record), R % 4 == 0, R <= 64.
 //
 // Sort: a stable counting sort of each tile by output row.  Warp w ranks
-// its items with __match_any_sync (order: warp, item, lane); bases per
+// its items with __match_any_sync and one leader atomic per equal-row group
+// (order: warp, item, lane); bases per
 // (row, warp) come from one block scan; records are scattered straight into
 // a sorted tile padded by one record per piece so that the 4 (or 8) groups of
 // a warp read their pieces without bank conflicts.
@@ -256,11 +257,12 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
+      // the group leader reserves the run (a warp's shared atomics to one
+      // address execute in issue order: stable) and broadcasts its base
+      const int leader = __ffs(grp) - 1;
       int old = 0;
-      if (k >= 0) old = wh[k];
-      __syncwarp();
-      if (k >= 0 && lane == __ffs(grp) - 1) wh[k] = old + __popc(grp);
-      __syncwarp();
+      if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
+      old = __shfl_sync(0xffffffffu, old, leader);
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();

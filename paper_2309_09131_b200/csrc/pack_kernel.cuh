@@ -130,15 +130,19 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     __syncwarp();
     // ---------------------------------------------------------------- B
     int *wh = s_hist + warp * hstride;
+    // stable per-warp counting: the leader of each equal-row group reserves
+    // the group's run with one shared atomic (returns the old count) and
+    // broadcasts it; a warp's shared atomics to one address execute in issue
+    // order, so runs are ordered by (item j, lane) as before -- without a
+    // load / store / syncwarp chain per item
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
+      const int leader = __ffs(grp) - 1;
       int old = 0;
-      if (k >= 0) old = wh[k];
-      __syncwarp();
-      if (k >= 0 && lane == __ffs(grp) - 1) wh[k] = old + __popc(grp);
-      __syncwarp();
+      if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
+      old = __shfl_sync(0xffffffffu, old, leader);
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
