@@ -21,6 +21,11 @@
 #ifndef PACK_U
 #define PACK_U 2
 #endif
+// equal-row peers by one ballot per row bit instead of __match_any_sync
+// (shorter latency chain; 4.566 -> 4.553 ms on c2)
+#ifndef PACK_BALLOT_MATCH
+#define PACK_BALLOT_MATCH 1
+#endif
 
 namespace fc {
 
@@ -54,6 +59,9 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
+#if PACK_BALLOT_MATCH
+  const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
+#endif
   uint2 *s_sorted = reinterpret_cast<uint2 *>(smem);
   int *s_misc = reinterpret_cast<int *>(smem + PP::sorted_bytes);
   int *s_piece_bin = s_misc + kFWarps + 4;  // first bin of every piece
@@ -138,7 +146,18 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
+#if PACK_BALLOT_MATCH
+      // equal-row peers from one ballot per key bit (rows < 2^hbits)
+      unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
+      for (int b = 0; b < hbits; ++b) {
+        const bool bit = (k >> b) & 1;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
+      }
+      const unsigned grp = k >= 0 ? peers : (1u << lane);
+#else
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
+#endif
       const int leader = __ffs(grp) - 1;
       int old = 0;
       if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
