@@ -21,6 +21,9 @@ idx = torch.stack([crd[:, 1], crd[:, 2]], dim=1).contiguous()
 n = idx.shape[0]
 L = ctypes.CDLL(str(Path(__file__).with_name("libgather_probe.so")))
 L.gather_probe.restype = ctypes.c_float
+L.gather_probe_tma.restype = ctypes.c_float
+L.gather_probe_tma.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 L.gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 sink = torch.zeros(1, device=dev)
@@ -30,3 +33,9 @@ for name, ix in (("layout order", idx), ("random order", idx[torch.randperm(n, d
             ms = L.gather_probe(ix.data_ptr(), n, fs.factors[1].data_ptr(), fs.factors[2].data_ptr(),
                                 sink.data_ptr(), u, blocks)
             print(f"{name:13s} U={u} blocks={blocks:5d}: {ms:.3f} ms  ({n * 256 / ms / 1e6:.0f} GB/s of rows)")
+
+for u in (4, 8):
+    for blocks in (148 * 2, 148 * 3, 148 * 8):
+        ms = L.gather_probe_tma(idx.data_ptr(), n, fs.factors[1].data_ptr(), fs.factors[2].data_ptr(),
+                                sink.data_ptr(), u, blocks)
+        print(f"TMA layout    U={u} blocks={blocks:5d}: {ms:.3f} ms  ({n * 256 / ms / 1e6:.0f} GB/s of rows)")
