@@ -339,12 +339,21 @@ class PeerShardedTensor:
                 _lib.call("fc_stream_signal", base + 4 * q, 0, st)
 
     def close(self):
+        """Unmap the peers' buffers (each GPU's own allocations are freed
+        when their IpcBuffer objects go; call after a barrier so no peer is
+        still using them)."""
         for ptr in self._opened:
             try:
                 _lib.call("fc_ipc_close", ptr)
             except Exception:
                 pass
         self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def peer_mttkrp_mode(dt: PeerShardedTensor, factors, mode: int) -> torch.Tensor:
