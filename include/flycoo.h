@@ -115,7 +115,12 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
  * fc_ipc_open (or this GPU's own buffer).  Replaces the send-region pass,
  * the NCCL all-to-all and fc_scatter_records.  npeers <= 8; nnz = local
  * element count (remap-only pass); the caller orders the passes of all GPUs
- * (barrier between modes). */
+ * (barrier between modes).  Heavy super-shards may be split across GPUs at
+ * chunk granularity: `chunk_owner[c]` names the GPU that owns chunk c's
+ * super-shard and the partial tile goes to its workspace peer_part_ws[owner]
+ * (partial ids are global); pass nred1 = nred2 = 0 and reduce on the owner
+ * with fc_reduce_partials after a barrier.  chunk_owner may be NULL (every
+ * chunk local). */
 int fc_mode_worker_peers(const void *src_crd, const float *src_val,
                          const float *const *factors, const int64_t *dims,
                          float *out, int nmodes, int mode, int rank,
@@ -128,7 +133,16 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val,
                          const uint32_t *dest_slots, int64_t nnz, int do_compute,
                          int acc_in_smem, int32_t *flags, unsigned long long *counters,
                          int npeers, void *const *peer_crd, float *const *peer_val,
-                         const int64_t *peer_base, void *stream);
+                         const int64_t *peer_base, float *const *peer_part_ws,
+                         const int32_t *chunk_owner, void *stream);
+
+/* K2 alone (the second half of fc_mode_worker): the deterministic two-level
+ * reduce of partial tiles into `out`.  Multi-GPU: the owner of super-shards
+ * whose chunks ran on several GPUs reduces the partials the peers wrote into
+ * its workspace, after a barrier. */
+int fc_reduce_partials(const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
+                       const float *part_ws, float *part_ws2, float *out, int64_t out_rows,
+                       int64_t m_mode, int rank, void *stream);
 
 /* Peer-memory plumbing for the fused exchange (no reference counterpart:
  * the reference is single-node shared memory).  IPC-shareable cudaMalloc

@@ -53,7 +53,9 @@ _SIGS = {
         _int, _int,                    # do_compute, acc_in_smem
         _vp, _vp,                      # flags, counters
         _int, _vp, _vp, _vp,           # npeers, peer_crd, peer_val (host arrays), peer_base (host)
+        _vp, _vp,                      # peer_part_ws (host array), chunk_owner (device int32)
         _vp]),                         # stream
+    "fc_reduce_partials": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "fc_ipc_handle_bytes": (_int, []),
     "fc_ipc_alloc": (_int, [_i64, _vp]),
     "fc_ipc_free": (_int, [_vp]),

@@ -20,6 +20,7 @@ struct PeerTable {
   int4 *crd[kMaxPeers];
   float *val[kMaxPeers];
   int64_t base[kMaxPeers + 1];
+  float *part_ws[kMaxPeers];  // partial-tile workspaces (super-shards split across GPUs)
 };
 
 // Owned output-row ranges of the GPUs (factor-row all-gather).
@@ -53,7 +54,16 @@ struct ModeArgs {
   int32_t *flags;
   unsigned long long *counters;
   PeerTable peers;
+  // multi-GPU: owner GPU of every chunk's super-shard (null: this GPU).  A
+  // super-shard whose chunks span GPUs gets its partial tiles written into
+  // the owner's workspace, which reduces them after a barrier.
+  const int32_t *chunk_owner;
 };
+
+// Partial-tile workspace of chunk c (indexed by the global partial id).
+__device__ __forceinline__ float *partial_ws(const ModeArgs &a, int64_t c) {
+  return a.chunk_owner ? a.peers.part_ws[a.chunk_owner[c]] : a.part_ws;
+}
 
 // Packed fp32 pairs: sm_100's FMUL2 / FFMA2 / FADD2 do two fp32 lanes per
 // instruction, each rounded exactly like the scalar op (bitwise-identical

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kBlock) mode_pass_kernel(const __grid_constant
   }
   __syncthreads();
   if constexpr (SMEM_ACC) {
-    float *dstp = part < 0 ? a.out + row0 * R : a.part_ws + (int64_t)part * a.m * R;
+    float *dstp = part < 0 ? a.out + row0 * R : partial_ws(a, chunk) + (int64_t)part * a.m * R;
     const int n = rows * R;
     if ((R & 3) == 0) {
       const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
@@ -498,7 +498,8 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
                             int64_t nred2, float *part_ws, float *part_ws2,
                             const uint32_t *dest_slots, int64_t nnz, int do_compute,
                             int do_remap, int acc_in_smem, int32_t *flags,
-                            unsigned long long *counters, void *stream, const PeerTable &peers) {
+                            unsigned long long *counters, void *stream, const PeerTable &peers,
+                            const int32_t *chunk_owner = nullptr) {
   FC_CHECK_ARG(nmodes >= 2 && nmodes <= 8, "nmodes %d outside [2, 8]", nmodes);
   FC_CHECK_ARG(mode >= 0 && mode < nmodes, "mode %d out of range", mode);
   FC_CHECK_ARG(src_crd && flags && counters, "null buffer");
@@ -579,6 +580,7 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
   a.flags = flags;
   a.counters = counters;
   a.peers = peers;
+  a.chunk_owner = chunk_owner;
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
   if (acc_in_smem && nred1 > 0) {
@@ -626,7 +628,8 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float 
                          const uint32_t *dest_slots, int64_t nnz, int do_compute,
                          int acc_in_smem, int32_t *flags, unsigned long long *counters,
                          int npeers, void *const *peer_crd, float *const *peer_val,
-                         const int64_t *peer_base, void *stream) {
+                         const int64_t *peer_base, float *const *peer_part_ws,
+                         const int32_t *chunk_owner, void *stream) {
   FC_CHECK_ARG(npeers >= 1 && npeers <= kMaxPeers, "npeers %d outside [1, %d]", npeers, kMaxPeers);
   FC_CHECK_ARG(peer_crd && peer_base && (dest_slots || nnz == 0), "null peer table");
   PeerTable t{};
@@ -641,13 +644,40 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float 
     t.base[q] = peer_base[q];
   }
   t.base[npeers] = peer_base[npeers];
+  FC_CHECK_ARG(!chunk_owner || peer_part_ws, "chunk owners need the peers' partial workspaces");
+  if (peer_part_ws)
+    for (int q = 0; q < npeers; ++q) t.part_ws[q] = peer_part_ws[q];
   for (int q = npeers + 1; q <= kMaxPeers; ++q) t.base[q] = t.base[npeers];
   FC_CHECK_ARG(t.base[npeers] <= (int64_t)UINT32_MAX + 1, "global slots exceed uint32");
   return mode_worker_impl(src_crd, src_val, nullptr, nullptr, factors, dims, out, nmodes, mode,
                           rank, out_rows, m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows,
                           tile_rows, hist_rows, nchunks, red1, nred1, red2, nred2, part_ws,
                           part_ws2, dest_slots, nnz, do_compute, 1, acc_in_smem, flags, counters,
-                          stream, t);
+                          stream, t, chunk_owner);
+}
+
+int fc_reduce_partials(const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
+                       const float *part_ws, float *part_ws2, float *out, int64_t out_rows,
+                       int64_t m_mode, int rank, void *stream) {
+  FC_CHECK_ARG(rank >= 1 && rank <= 256, "rank %d outside [1, 256]", rank);
+  FC_CHECK_ARG(m_mode >= 1 && out_rows >= 1 && out, "bad output geometry");
+  cudaStream_t st = as_stream(stream);
+  const int64_t cells = m_mode * rank;
+  const unsigned gy = (unsigned)((cells + 255) / 256);
+  FC_CHECK_ARG(gy < 65536, "super-shard tile too large for the reduce grid");
+  if (nred1 > 0) {
+    FC_CHECK_ARG(red1 && part_ws, "null reduce plan");
+    reduce_level_kernel<<<dim3((unsigned)nred1, gy), 256, 0, st>>>(red1, 4, part_ws, part_ws2, out,
+                                                                   out_rows, m_mode, rank);
+    FC_LAUNCH_CHECK();
+  }
+  if (nred2 > 0) {
+    FC_CHECK_ARG(red2 && part_ws2, "null level-2 reduce plan");
+    reduce_level_kernel<<<dim3((unsigned)nred2, gy), 256, 0, st>>>(red2, 3, part_ws2, nullptr, out,
+                                                                   out_rows, m_mode, rank);
+    FC_LAUNCH_CHECK();
+  }
+  return FC_OK;
 }
 
 int fc_remap_cursor(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,

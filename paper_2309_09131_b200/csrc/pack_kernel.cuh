@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   }
   if (!direct) {
     __syncthreads();
-    float *dstp = part < 0 ? out_rows : a.part_ws + (int64_t)part * a.m * R;
+    float *dstp = part < 0 ? out_rows : partial_ws(a, chunk) + (int64_t)part * a.m * R;
     const int n4 = rows * R / 4;
     const float4 *s4 = reinterpret_cast<const float4 *>(s_acc);
     float4 *d4 = reinterpret_cast<float4 *>(dstp);

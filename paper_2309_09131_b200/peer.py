@@ -1,28 +1,31 @@
 """Multi-GPU sweep with the remap fused into the exchange.
 
-Same partition as :mod:`dist` -- per mode, GPU p owns a contiguous
-super-shard range and the matching contiguous slice [E_p, E_{p+1}) of the
-single-GPU mode-n buffer -- but no send region, all-to-all or unpack pass:
+Partition.  GPUs take contiguous ranges of the single-GPU chunk list of each
+mode (the same CTA chunks, partial-tile ids and K2 reduce plan as one GPU),
+balanced by nonzeros -- so a Zipf head super-shard (c2: ~40% of a mode) is
+split across GPUs instead of capping the speed-up.  Every super-shard's
+rows stay owned by ONE GPU (the one running its first chunk), so each GPU
+still owns a contiguous output-row range per mode (north_star); chunks of a
+split super-shard write their partial tiles into the owner's workspace and
+the owner reduces them in the single-GPU order -- outputs are bitwise
+identical to the single-GPU sweep.
 
-* every GPU's record buffers (and its per-mode output rows) are cudaMalloc
-  allocations shared with all peers through CUDA IPC, mapped over NVLink;
-* the mode pass (``fc_mode_worker_peers``) reads the element's GLOBAL
-  mode-(n+1) slot d from the single-GPU slot map and stores the record
-  straight into the back buffer of the owner q of d (E'_q <= d < E'_{q+1})
-  at d - E'_q: the NVLink transfer overlaps the compute tile by tile, and a
-  remote record crosses the fabric exactly once;
-* after a barrier, each GPU pulls the peers' owned rows of the updated
-  factor from their output buffers (copy engines over NVLink) -- the
-  all-gather of engine.sweep_all_modes' factor replacement (engine.py:292).
+Exchange.  Every GPU's record buffers, partial workspace and per-mode output
+rows are cudaMalloc allocations shared through CUDA IPC and mapped over
+NVLink.  The mode pass (``fc_mode_worker_peers``) reads the element's
+GLOBAL mode-(n+1) slot d from the single-GPU slot map and stores the record
+straight into the back buffer of the owner q of d (E'_q <= d < E'_{q+1}) at
+d - E'_q: the NVLink transfer overlaps the compute tile by tile and a remote
+record crosses the fabric once -- no send region, all-to-all or unpack pass.
 
-Between modes the GPUs order themselves on the device: each sets a
-per-mode flag in every peer's memory with a stream write (fenced after its
-pass), waits for all peers' flags with stream waits and resets them -- "all peers
-finished writing my back buffer / reading their front buffer" -- without a
-host round trip or any SM spinning (``FLYCOO_PEER_SYNC=host``: stream
-synchronize + ``dist.barrier``).  After every mode each
-GPU's slice equals the single-GPU buffer's slice bit-exactly
-(tests/test_gpu_peer.py).
+Ordering.  Per mode: K1 -> barrier (peers' partials are in) -> K2 of the
+owned super-shards -> barrier (owned rows final) -> one kernel gathers the
+peers' owned rows over NVLink (the factor all-gather of engine.py:292).  The
+barriers run on the device: each GPU sets a flag in every peer's memory with
+a fenced stream write and waits for its own flags with stream waits (no host
+round trip, no SM spinning; ``FLYCOO_PEER_SYNC=host``: stream synchronize +
+``dist.barrier``).  The flag values are constants, so a whole sweep is
+captured as one CUDA graph per GPU (:class:`PeerSweepGraph`).
 """
 
 from __future__ import annotations
@@ -36,42 +39,115 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .dist import _local_plan, partition_super_shards
-from .layout import DeviceShardedTensor, PartitionPlan, default_chunk_elems, make_mode_work
+from .layout import DeviceShardedTensor, PartitionPlan, make_mode_work
 
-__all__ = ["PeerModePlan", "peer_plans", "IpcBuffer", "PeerShardedTensor", "peer_mttkrp_mode",
-           "peer_sweep_all_modes", "PeerSweepGraph"]
+__all__ = ["PeerModePlan", "partition_chunks", "super_shard_owners", "peer_plans", "IpcBuffer",
+           "PeerShardedTensor", "peer_mttkrp_mode", "peer_sweep_all_modes", "PeerSweepGraph"]
 
 
 @dataclass
 class PeerModePlan:
-    ss_lo: int
-    ss_hi: int
-    e_lo: int
+    """One GPU's share of one mode pass.  GPUs take contiguous ranges of the
+    single-GPU chunk list (balanced by nonzeros), so a heavy super-shard's
+    chunks may run on several GPUs; its rows stay owned by ONE GPU (the one
+    running its first chunk), which reduces all its partial tiles."""
+    c_lo: int                   # chunk range [c_lo, c_hi) of the global plan
+    c_hi: int
+    e_lo: int                   # element range = chunk_start[c_lo], chunk_start[c_hi]
     e_hi: int
+    ss_lo: int                  # owned super-shards [ss_lo, ss_hi)
+    ss_hi: int
     global_slots: torch.Tensor  # int32 (uint32 bits): global mode-(n+1) positions
-    peer_base: list             # world + 1 element bounds of mode n+1
+    peer_base: list             # world + 1 element bounds of mode n+1 (owner of a slot)
+    row_bounds: list            # world + 1 owned-row bounds of mode n
+    chunk_owner: torch.Tensor   # int32 per chunk of [c_lo, c_hi): GPU owning its super-shard
+    red1: torch.Tensor          # K2 tasks of the owned super-shards
+    red2: torch.Tensor
 
     @property
     def count(self) -> int:
         return self.e_hi - self.e_lo
 
 
-def peer_plans(plan: PartitionPlan, slot_maps, world: int, rank: int):
-    """Per-mode plan of `rank`: its element slice, the slot-map slice (global
-    destinations) and the next mode's ownership bounds.  Returns
-    (plans, bounds, cap) like dist.build_rank_plans."""
+def partition_chunks(chunk_start: np.ndarray, world: int) -> np.ndarray:
+    """world + 1 chunk bounds splitting the chunk list into contiguous ranges
+    of ~equal nonzero counts."""
+    nch = chunk_start.shape[0] - 1
+    total = int(chunk_start[-1] - chunk_start[0])
+    cb = [0]
+    for p in range(1, world):
+        target = chunk_start[0] + p * total / world
+        c = int(np.searchsorted(chunk_start[:nch], target, side="left"))
+        cb.append(min(max(c, cb[-1]), nch))
+    cb.append(nch)
+    return np.asarray(cb, dtype=np.int64)
+
+
+def super_shard_owners(work, k: int, m: int, chunk_gpu: np.ndarray, world: int) -> np.ndarray:
+    """Owner GPU of every super-shard: the GPU running the first chunk that
+    covers it (a direct chunk covers several); super-shards without chunks
+    (empty, zeroed by K2) go to the owner of the next covered one."""
+    cs = work.chunk_ss.cpu().numpy().astype(np.int64)
+    cp = work.chunk_part.cpu().numpy()
+    if work.chunk_rows is not None:
+        cr = work.chunk_rows.cpu().numpy().astype(np.int64)
+        nss = np.where(cp == -2, -(-cr // m), 1)
+    else:
+        nss = np.ones_like(cs)
+    ss_cov = np.repeat(cs, nss) + (np.arange(int(nss.sum())) -
+                                   np.repeat(np.concatenate(([0], np.cumsum(nss)))[:-1], nss))
+    gpu_cov = np.repeat(chunk_gpu, nss)
+    owner = np.full(k, -1, dtype=np.int64)
+    if ss_cov.size:
+        idx = np.searchsorted(ss_cov, np.arange(k), side="left")
+        ok = idx < ss_cov.size
+        ok[ok] = ss_cov[idx[ok]] == np.arange(k)[ok]
+        owner[ok] = gpu_cov[idx[ok]]
+    nxt = world - 1  # backward fill of uncovered super-shards
+    for s in range(k - 1, -1, -1):
+        if owner[s] < 0:
+            owner[s] = nxt
+        else:
+            nxt = owner[s]
+    assert np.all(np.diff(owner) >= 0), "super-shard owners must be monotone"
+    return owner
+
+
+def peer_plans(plan: PartitionPlan, slot_maps, world: int, rank: int, R: int, device):
+    """Per-mode plans of `rank` on the global single-GPU work plans (one per
+    mode, rank R).  Returns (plans, works, cap): cap = the largest element
+    slice of any GPU in any mode (record buffer rows)."""
     N = plan.num_modes
-    bounds = [partition_super_shards(plan.ss_counts[n], world) for n in range(N)]
-    cap = max(int(bounds[n][1][p + 1] - bounds[n][1][p]) for n in range(N) for p in range(world))
+    works, cbs = [], []
+    for n in range(N):
+        w = make_mode_work(plan, n, R, device)
+        works.append(w)
+        cbs.append(partition_chunks(w.chunk_start.cpu().numpy(), world))
+    starts = [w.chunk_start.cpu().numpy() for w in works]
+    ebs = [starts[n][cbs[n]] for n in range(N)]
+    cap = max(int(eb[p + 1] - eb[p]) for eb in ebs for p in range(world))
     plans = []
     for n in range(N):
-        sb, eb = bounds[n]
-        lo, hi = int(eb[rank]), int(eb[rank + 1])
-        base = [int(x) for x in bounds[(n + 1) % N][1]]
-        plans.append(PeerModePlan(int(sb[rank]), int(sb[rank + 1]), lo, hi,
-                                  slot_maps[n][lo:hi].to(torch.int32).clone(), base))
-    return plans, bounds, max(cap, 1)
+        w, cb, eb = works[n], cbs[n], ebs[n]
+        m, k, dim = int(plan.params.m[n]), int(plan.params.k[n]), int(plan.params.dims[n])
+        chunk_gpu = np.repeat(np.arange(world), np.diff(cb))
+        owner = super_shard_owners(w, k, m, chunk_gpu, world)
+        lo_ss = [int(np.searchsorted(owner, p, side="left")) for p in range(world)] + [k]
+        rows = [min(x * m, dim) for x in lo_ss]
+        cs = w.chunk_ss.cpu().numpy().astype(np.int64)
+        c_lo, c_hi = int(cb[rank]), int(cb[rank + 1])
+        r1 = w.red1.cpu().numpy().reshape(-1, 4)
+        r2 = w.red2.cpu().numpy().reshape(-1, 3)
+        r1 = r1[owner[r1[:, 0]] == rank] if r1.size else r1
+        r2 = r2[owner[r2[:, 0]] == rank] if r2.size else r2
+        e_lo, e_hi = int(eb[rank]), int(eb[rank + 1])
+        t = lambda a, dt=torch.int64: torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(device)
+        plans.append(PeerModePlan(
+            c_lo, c_hi, e_lo, e_hi, lo_ss[rank], lo_ss[rank + 1],
+            slot_maps[n][e_lo:e_hi].to(torch.int32).clone().to(device),
+            [int(x) for x in ebs[(n + 1) % N]], rows,
+            t(owner[cs[c_lo:c_hi]], torch.int32), t(r1), t(r2)))
+    return plans, works, max(cap, 1)
 
 
 class IpcBuffer:
@@ -121,17 +197,20 @@ class PeerShardedTensor:
     per GPU): buffers are IPC allocations and :meth:`connect` maps the peers'
     through torch.distributed; ``ipc=False``: ordinary device tensors, peers
     wired by :meth:`connect_local` (several virtual ranks in one process --
-    the single-GPU parity test of the peer-store kernel path)."""
+    the single-GPU parity test of the peer-store kernel path).  `R` is the
+    factor rank the work plans are built for (default: the params' rank)."""
 
     def __init__(self, st: DeviceShardedTensor, world: int, rank: int, group=None,
-                 ipc: bool = True):
+                 ipc: bool = True, R: int | None = None):
         if world > 8:
             raise ValueError("the fused exchange maps at most 8 peers")
         self.plan = st.plan
         self.world, self.rank, self.group, self.ipc = world, rank, group, ipc
         self.device = st.device
         self.num_modes = st.num_modes
-        self.plans, self.bounds, self.cap = peer_plans(st.plan, st.slot_maps, world, rank)
+        self.R = int(R if R is not None else st.plan.params.rank)
+        self.plans, self.works, self.cap = peer_plans(st.plan, st.slot_maps, world, rank,
+                                                      self.R, st.device)
         cw = st.crd[0].shape[1]
         self.cw = cw
         emb = st.val[0] is None
@@ -143,23 +222,31 @@ class PeerShardedTensor:
         self.crd[0][:p0.count] = st.crd[st.active][p0.e_lo:p0.e_hi]
         if not emb:
             self.val[0][:p0.count] = st.val[st.active][p0.e_lo:p0.e_hi]
+        # partial tiles, indexed by the global partial id: peers write the
+        # partials of super-shards this GPU owns into it (one buffer for all
+        # modes: a mode's partials are reduced before any GPU starts the next)
+        ws = max([w.part_ws.numel() for w in self.works if w.part_ws is not None] + [1])
+        self.part_ws = self._alloc((ws,), torch.float32)
+        for w in self.works:
+            w.part_ws = None
         self.active = 0
         self.active_mode = 0
         self.peer_crd = None     # [buffer k][rank q] -> device pointer
         self.peer_val = None
+        self.peer_part_ws = None
         self.outs = {}           # (mode, R) -> (tensor, [peer pointers])
-        self._work = {}
         self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._expected = 0
         self._opened = []
-        # cross-GPU ordering between passes (stream memory operations, no host
-        # round trip): flags[n][q] = 1 once GPU q finished its mode-n pass;
-        # reset to 0 by this GPU after its wait.  Constant values make the
-        # protocol replayable in a CUDA graph; a peer's next signal on the same
-        # slot always follows this GPU's reset (it first waits on a later
-        # mode's signal of ours).  FLYCOO_PEER_SYNC=host: stream synchronize +
-        # dist.barrier instead.
-        self.flags = self._alloc((self.num_modes, world), torch.int32)
+        # cross-GPU ordering (stream memory operations, no host round trip):
+        # two barriers per mode (after K1: peers' partial tiles are in; after
+        # K2: owned rows are final).  flags[b][q] = 1 once GPU q reached
+        # barrier b, reset to 0 by this GPU after its wait; constant values
+        # make the protocol replayable in a CUDA graph, and a peer's next set
+        # of the same slot always follows this GPU's reset (it first waits on
+        # a later barrier of ours).  FLYCOO_PEER_SYNC=host: stream synchronize
+        # + dist.barrier instead.
+        self.flags = self._alloc((2 * self.num_modes, world), torch.int32)
         self.peer_flags = None
         self.device_sync = ipc and os.environ.get("FLYCOO_PEER_SYNC", "device") != "host"
 
@@ -195,11 +282,12 @@ class PeerShardedTensor:
         return out
 
     def connect(self):
-        """Collective over the group: map every peer's record buffers and
-        barrier flags."""
-        ptrs = self._exchange_ptrs(self._shared() + [self.flags])
+        """Collective over the group: map every peer's record buffers,
+        partial-tile workspace and barrier flags."""
+        ptrs = self._exchange_ptrs(self._shared() + [self.part_ws, self.flags])
         self.peer_crd = [ptrs[0], ptrs[1]]
         self.peer_val = None if self.val[0] is None else [ptrs[2], ptrs[3]]
+        self.peer_part_ws = ptrs[-2]
         self.peer_flags = ptrs[-1]
 
     @staticmethod
@@ -209,12 +297,12 @@ class PeerShardedTensor:
             dt.peer_crd = [[r.crd[k].data_ptr() for r in ranks] for k in range(2)]
             dt.peer_val = None if dt.val[0] is None else [[r.val[k].data_ptr() for r in ranks]
                                                           for k in range(2)]
+            dt.peer_part_ws = [r.part_ws.data_ptr() for r in ranks]
             dt._local_ranks = ranks
 
     def output(self, mode: int, R: int):
-        """Persistent, peer-visible output rows of `mode` (every row is
-        rewritten by each pass: owned rows by the pass, the rest by the
-        pull)."""
+        """Persistent, peer-visible output rows of `mode` (owned rows are
+        rewritten by every pass, the rest by the row gather)."""
         key = (mode, R)
         if key not in self.outs:
             t = self._alloc((self.plan.params.dims[mode], R), torch.float32)
@@ -232,62 +320,76 @@ class PeerShardedTensor:
         v = None if self.val[self.active] is None else self.val[self.active][:p.count]
         return c, v
 
-    def mode_work(self, mode: int, R: int):
-        key = (mode, R)
-        if key not in self._work:
-            lp = _local_plan(self.plan, mode, self.plans[mode])
-            p = self.plans[mode]
-            self._work[key] = make_mode_work(lp, mode, R, self.device,
-                                             chunk_elems=default_chunk_elems(self.plan.nnz),
-                                             ss_range=(p.ss_lo, p.ss_hi))
-        return self._work[key]
+    def mode_work(self, mode: int, R: int | None = None):
+        """The global single-GPU work plan of `mode` (this GPU runs a chunk
+        range of it)."""
+        return self.works[mode]
 
     def owned_rows(self, mode: int):
-        p = self.plans[mode]
-        m = self.plan.params.m[mode]
-        dim = self.plan.params.dims[mode]
-        return min(p.ss_lo * m, dim), min(p.ss_hi * m, dim)
+        rb = self.plans[mode].row_bounds
+        return rb[self.rank], rb[self.rank + 1]
 
     def row_ranges(self, mode: int):
-        m = self.plan.params.m[mode]
-        dim = self.plan.params.dims[mode]
-        sb = self.bounds[mode][0]
-        return [(min(int(sb[q]) * m, dim), min(int(sb[q + 1]) * m, dim)) for q in range(self.world)]
+        rb = self.plans[mode].row_bounds
+        return [(rb[q], rb[q + 1]) for q in range(self.world)]
 
     # -- passes
     def mode_pass(self, factors, mode: int, out: torch.Tensor, stream=None):
-        """Fused K1 (+K2) of this rank: compute owned rows into `out`, store
-        every record into its owner's back buffer."""
+        """K1 over this GPU's chunk range: rows of owned super-shards that
+        need no reduce into `out`, partial tiles into their owners'
+        workspaces, every record into its owner's back buffer."""
         if self.peer_crd is None:
             raise RuntimeError("peers not connected (connect / connect_local)")
         p = self.plans[mode]
         R = int(out.shape[1])
-        w = self.mode_work(mode, R)
+        if R != self.R:
+            raise ValueError(f"work plans were built for rank {self.R}, factors have {R}")
+        w = self.works[mode]
         a, b = self.active, 1 - self.active
-        vp = lambda t: t.data_ptr() if t is not None else None
         params = self.plan.params
         stat = self._stat.data_ptr()
-        pv = None if self.peer_val is None else _lib.ptr_array(self.peer_val[b])
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-        _lib.call("fc_mode_worker_peers", self.crd[a].data_ptr(), vp(self.val[a]),
+        c0 = p.c_lo
+        # global element / chunk indices address this GPU's slices directly
+        src = self.crd[a].data_ptr() - p.e_lo * self.cw * 4
+        srcv = None if self.val[a] is None else self.val[a].data_ptr() - p.e_lo * 4
+        slots = p.global_slots.data_ptr() - p.e_lo * 4
+        pv = None if self.peer_val is None else _lib.ptr_array(self.peer_val[b])
+        _lib.call("fc_mode_worker_peers", src, srcv,
                   _lib.ptr_array([f.data_ptr() for f in factors]), _lib.i64_array(params.dims),
                   out.data_ptr(), self.num_modes, mode, R, params.dims[mode], params.m[mode],
-                  w.chunk_start.data_ptr(), w.chunk_ss.data_ptr(), w.chunk_part.data_ptr(),
-                  vp(w.chunk_rows), w.tile_rows, w.hist_rows, w.nchunks, w.red1.data_ptr(),
-                  w.nred1, w.red2.data_ptr(), w.nred2, vp(w.part_ws), vp(w.part_ws2),
-                  p.global_slots.data_ptr(), p.count, 1, int(w.acc_in_smem), stat + 8, stat,
-                  self.world, _lib.ptr_array(self.peer_crd[b]), pv, _lib.i64_array(p.peer_base),
-                  st)
+                  w.chunk_start.data_ptr() + 8 * c0, w.chunk_ss.data_ptr() + 4 * c0,
+                  w.chunk_part.data_ptr() + 4 * c0,
+                  None if w.chunk_rows is None else w.chunk_rows.data_ptr() + 4 * c0,
+                  w.tile_rows, w.hist_rows, p.c_hi - c0, None, 0, None, 0,
+                  self.part_ws.data_ptr(), None, slots, p.count, 1, int(w.acc_in_smem),
+                  stat + 8, stat, self.world, _lib.ptr_array(self.peer_crd[b]), pv,
+                  _lib.i64_array(p.peer_base), _lib.ptr_array(self.peer_part_ws),
+                  p.chunk_owner.data_ptr() if p.chunk_owner.numel() else None, st)
         self._expected += p.count
 
+    def reduce(self, mode: int, out: torch.Tensor, stream=None):
+        """K2 of the owned super-shards (after the post-K1 barrier)."""
+        p = self.plans[mode]
+        w = self.works[mode]
+        n1, n2 = int(p.red1.shape[0]), int(p.red2.shape[0])
+        if n1 == 0 and n2 == 0:
+            return
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        params = self.plan.params
+        _lib.call("fc_reduce_partials", p.red1.data_ptr() if n1 else None, n1,
+                  p.red2.data_ptr() if n2 else None, n2, self.part_ws.data_ptr(),
+                  None if w.part_ws2 is None else w.part_ws2.data_ptr(), out.data_ptr(),
+                  params.dims[mode], params.m[mode], int(out.shape[1]), st)
+
     def pull_rows(self, mode: int, out: torch.Tensor, peer_out_ptrs, stream=None):
-        """Copy the peers' owned rows of `mode` into `out` (NVLink copy
-        engines); `out` then holds the whole updated factor."""
+        """Gather the peers' owned rows of `mode` into `out` (one kernel,
+        NVLink loads); `out` then holds the whole updated factor."""
         R = int(out.shape[1])
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         ranges = self.row_ranges(mode)
         bounds = [lo for lo, _ in ranges] + [ranges[-1][1]]
-        if R % 4 == 0:  # one launch, NVLink loads
+        if R % 4 == 0:
             _lib.call("fc_gather_peer_rows", out.data_ptr(), _lib.ptr_array(peer_out_ptrs),
                       _lib.i64_array(bounds), self.world, self.rank, R, st)
             return
@@ -320,23 +422,32 @@ class PeerShardedTensor:
         if self.ipc:
             dist.barrier(group=self.group)
 
-    def sync(self, mode: int = 0):
-        """Order the GPUs after the mode-`mode` pass: afterwards every peer's
-        pass (records stored into this GPU, owned output rows) is complete
-        and visible, and no peer still reads this GPU's front buffer."""
+    def sync(self, slot: int = 0):
+        """Device barrier `slot` (2n: after mode n's K1, 2n + 1: after its
+        K2): afterwards every peer's work before its own barrier `slot` is
+        complete and visible to this GPU."""
         if not self.device_sync:
             self.barrier()
             return
         st = torch.cuda.current_stream().cuda_stream
-        slot = 4 * mode * self.world
+        off = 4 * slot * self.world
         for q in range(self.world):
             if q != self.rank:
-                _lib.call("fc_stream_signal", self.peer_flags[q] + slot + 4 * self.rank, 1, st)
-        base = self.flags.data_ptr() + slot
+                _lib.call("fc_stream_signal", self.peer_flags[q] + off + 4 * self.rank, 1, st)
+        base = self.flags.data_ptr() + off
         for q in range(self.world):
             if q != self.rank:
                 _lib.call("fc_stream_wait", base + 4 * q, 1, st)
                 _lib.call("fc_stream_signal", base + 4 * q, 0, st)
+
+    def full_pass(self, factors, mode: int, out: torch.Tensor, peer_out_ptrs):
+        """K1, barrier, K2 (owned super-shards), barrier, row gather, swap."""
+        self.mode_pass(factors, mode, out)
+        self.sync(2 * mode)
+        self.reduce(mode, out)
+        self.sync(2 * mode + 1)
+        self.pull_rows(mode, out, peer_out_ptrs)
+        self.swap()
 
     def close(self):
         """Unmap the peers' buffers (each GPU's own allocations are freed
@@ -359,15 +470,12 @@ class PeerShardedTensor:
 def peer_mttkrp_mode(dt: PeerShardedTensor, factors, mode: int) -> torch.Tensor:
     """One fused mode pass across the group; returns this rank's persistent
     output of `mode` with every row valid (owned rows computed here, the
-    rest pulled from the peers)."""
+    rest gathered from the peers)."""
     if dt.active_mode != mode:
         raise ValueError(f"active mode is {dt.active_mode}, not {mode}")
     R = int(factors[0].shape[1])
     out, ptrs = dt.output(mode, R)
-    dt.mode_pass(factors, mode, out)
-    dt.sync(mode)
-    dt.pull_rows(mode, out, ptrs)
-    dt.swap()
+    dt.full_pass(factors, mode, out, ptrs)
     return out
 
 
@@ -429,10 +537,7 @@ class PeerSweepGraph:
                 working = list(self.inputs)
                 for n in range(self.N):
                     out, ptrs = dt.output(n, self.R)
-                    dt.mode_pass(working, n, out)
-                    dt.sync(n)
-                    dt.pull_rows(n, out, ptrs)
-                    dt.swap()
+                    dt.full_pass(working, n, out, ptrs)
                     working[n] = out
         torch.cuda.current_stream().wait_stream(side)
         expected = dt._expected - saved[2]

@@ -15,8 +15,9 @@ from paper_2309_09131_b200.peer import PeerShardedTensor, peer_plans
 from test_dist import _case, _global_records
 
 
-def _emulated_pass(ranks, r, factors, mode, out):
-    """K1 of virtual rank r: owned rows of `out` + peer stores."""
+def _emulated_pass(ranks, r, factors, mode, contrib):
+    """K1 of virtual rank r: its chunks' contributions to the output rows
+    (into `contrib`, full size) + peer stores of every record."""
     dt = ranks[r]
     p = dt.plans[mode]
     a, b = dt.active, 1 - dt.active
@@ -27,9 +28,7 @@ def _emulated_pass(ranks, r, factors, mode, out):
     for w in range(N):
         if w != mode:
             t = t * factors[w][recs[:, w].long()]
-    lo, hi = dt.owned_rows(mode)
-    out[lo:hi] = 0
-    out.index_add_(0, recs[:, mode].long(), t.to(out.dtype))
+    contrib.index_add_(0, recs[:, mode].long(), t.to(contrib.dtype))
     d = p.global_slots.long() & 0xFFFFFFFF
     base = torch.tensor(p.peer_base)
     q = torch.searchsorted(base, d, right=True) - 1
@@ -51,22 +50,20 @@ def test_peer_sweep_virtual_ranks_cpu(world, N):
         slot_maps=[torch.from_numpy(s.astype(np.int64)) for s in d.slot_maps],
         crd=[torch.from_numpy(rec0), None],
         val=[None if val0 is None else torch.from_numpy(val0), None])
-    ranks = [PeerShardedTensor(st, world, r, ipc=False) for r in range(world)]
+    ranks = [PeerShardedTensor(st, world, r, ipc=False, R=8) for r in range(world)]
     rng = np.random.default_rng(9)
     f0 = [torch.from_numpy(rng.random((dd, 8))) for dd in dims]
     working = [list(f0) for _ in range(world)]
-    outs = {n: [torch.zeros((dims[n], 8), dtype=torch.float64) for _ in range(world)]
-            for n in range(N)}
     for n in range(N):
+        contrib = [torch.zeros((dims[n], 8), dtype=torch.float64) for _ in range(world)]
         for r in range(world):
-            _emulated_pass(ranks, r, working[r], n, outs[n][r])
+            _emulated_pass(ranks, r, working[r], n, contrib[r])
+        total = sum(contrib)  # owners reduce split super-shards; the gather spreads rows
+        rb = ranks[0].plans[n].row_bounds
+        assert rb[0] == 0 and rb[-1] == dims[n] and all(x <= y for x, y in zip(rb, rb[1:]))
         for r, dt in enumerate(ranks):
-            # the pull: peers' owned rows into this rank's output
-            for q, (lo, hi) in enumerate(dt.row_ranges(n)):
-                if q != r:
-                    outs[n][r][lo:hi] = outs[n][q][lo:hi]
             dt.swap()
-            working[r][n] = outs[n][r]
+            working[r][n] = total.clone()
         nxt = (n + 1) % N
         want, wval = _global_records(subs, vals, d.orders[nxt], N)
         for r, dt in enumerate(ranks):
@@ -87,7 +84,7 @@ def test_peer_plans_cover_every_slot_once():
     dims, subs, vals, params, L, d, plan = _case(3)
     slot_maps = [torch.from_numpy(s.astype(np.int64)) for s in d.slot_maps]
     for world in (1, 2, 5, 8):
-        per_rank = [peer_plans(plan, slot_maps, world, r)[0] for r in range(world)]
+        per_rank = [peer_plans(plan, slot_maps, world, r, 8, "cpu")[0] for r in range(world)]
         for n in range(3):
             base = per_rank[0][n].peer_base
             assert len(base) == world + 1 and base[0] == 0 and base[-1] == len(vals)
@@ -95,6 +92,11 @@ def test_peer_plans_cover_every_slot_once():
             assert torch.equal(torch.sort(allslots).values, torch.arange(len(vals)))
             # every rank's bounds are the same static table
             assert all(pr[n].peer_base == base for pr in per_rank)
+            # chunk ranges tile the chunk list; each super-shard has one owner
+            assert per_rank[0][n].c_lo == 0
+            for a, b in zip(per_rank, per_rank[1:]):
+                assert a[n].c_hi == b[n].c_lo and a[n].ss_hi == b[n].ss_lo
+            assert per_rank[-1][n].ss_hi == params.k[n]
 
 
 def test_peer_world_limit():
@@ -103,3 +105,31 @@ def test_peer_world_limit():
                                slot_maps=[torch.zeros(1)] * 3, crd=[None, None], val=[None, None])
     with pytest.raises(ValueError, match="at most 8"):
         PeerShardedTensor(st, 9, 0, ipc=False)
+
+
+def test_chunk_partition_balances_a_heavy_super_shard():
+    """A super-shard holding most nonzeros is split across GPUs at chunk
+    granularity; its rows (and K2 tasks) stay with the GPU of its first chunk."""
+    from paper_2309_09131_b200.layout import make_mode_work, plan_from_counts
+    from paper_2309_09131_b200.params import device_params
+    from paper_2309_09131_b200.peer import partition_chunks, super_shard_owners
+    dims = (640, 50, 50)
+    rng = np.random.default_rng(3)
+    n0, n1 = 30_000, 20_000  # ~60% of the nonzeros in super-shard 0 (rows < 64)
+    c0 = np.stack([rng.integers(0, 64, n0), rng.integers(0, 50, n0), rng.integers(0, 50, n0)], 1)
+    c1 = np.stack([rng.integers(64, 640, n1), rng.integers(0, 50, n1), rng.integers(0, 50, n1)], 1)
+    subs = np.unique(np.concatenate([c0, c1]), axis=0)
+    params = device_params(dims, len(subs), 8, g=1024, m=[64, 16, 16])
+    counts = [np.bincount(subs[:, w] // params.m[w], minlength=params.k[w]) for w in range(3)]
+    plan = plan_from_counts(params, counts)
+    w = make_mode_work(plan, 0, 8, "cpu", chunk_elems=2048)
+    cs = w.chunk_start.numpy()
+    for world in (2, 4, 8):
+        cb = partition_chunks(cs, world)
+        loads = np.diff(cs[cb])
+        assert loads.max() <= len(subs) / world + 2048, (world, loads)
+        gpu = np.repeat(np.arange(world), np.diff(cb))
+        owner = super_shard_owners(w, params.k[0], 64, gpu, world)
+        assert owner[0] == 0 and np.all(np.diff(owner) >= 0)
+        # the heavy super-shard's chunks run on several GPUs
+        assert len(set(gpu[w.chunk_ss.numpy() == 0])) > 1
