@@ -353,7 +353,7 @@ class PeerShardedTensor:
         # global element / chunk indices address this GPU's slices directly
         src = self.crd[a].data_ptr() - p.e_lo * self.cw * 4
         srcv = None if self.val[a] is None else self.val[a].data_ptr() - p.e_lo * 4
-        slots = p.global_slots.data_ptr() - p.e_lo * 4
+        slots = p.global_slots.data_ptr() - p.e_lo * 4 if p.count else None
         pv = None if self.peer_val is None else _lib.ptr_array(self.peer_val[b])
         _lib.call("fc_mode_worker_peers", src, srcv,
                   _lib.ptr_array([f.data_ptr() for f in factors]), _lib.i64_array(params.dims),
