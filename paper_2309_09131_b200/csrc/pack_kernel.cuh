@@ -13,13 +13,13 @@
 
 #include "fast_kernel.cuh"
 
-// 4 CTAs/SM (its shared footprint is ~36 KB), 2 elements in flight per
+// 4 CTAs/SM (its shared footprint is ~36 KB), 3 elements in flight per
 // group: no spills at the 64-register cap (profiles/r1_kernel_experiments.md)
 #ifndef PACK_MIN_BLOCKS
 #define PACK_MIN_BLOCKS 4
 #endif
 #ifndef PACK_U
-#define PACK_U 2
+#define PACK_U 3
 #endif
 // equal-row peers by one ballot per row bit instead of __match_any_sync
 // (shorter latency chain; 4.566 -> 4.553 ms on c2)
