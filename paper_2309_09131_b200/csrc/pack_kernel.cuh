@@ -26,6 +26,16 @@
 #ifndef PACK_BALLOT_MATCH
 #define PACK_BALLOT_MATCH 1
 #endif
+// phase C: a window of U elements that lies inside the current row skips the
+// per-element row-change test (no branch / reconvergence per element)
+#ifndef PACK_FASTWIN
+#define PACK_FASTWIN 1
+#endif
+// phase D: one warp per tail entry folds the head entries that continue its
+// row (no scans over empty entries, no zeroing of the boundary tiles)
+#ifndef PACK_SIMPLE_D
+#define PACK_SIMPLE_D 1
+#endif
 
 namespace fc {
 
@@ -149,10 +159,13 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #if PACK_BALLOT_MATCH
       // equal-row peers from one ballot per key bit (rows < 2^hbits)
       unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
-      for (int b = 0; b < hbits; ++b) {
-        const bool bit = (k >> b) & 1;
-        const unsigned m = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? m : ~m;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // rows <= 256; the guard is warp-uniform
+        if (b < hbits) {
+          const bool bit = (k >> b) & 1;
+          const unsigned m = __ballot_sync(0xffffffffu, bit);
+          peers &= bit ? m : ~m;
+        }
       }
       const unsigned grp = k >= 0 ? peers : (1u << lane);
 #else
@@ -223,11 +236,13 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       s_bnd_row[2 * gi] = -1;
       s_bnd_row[2 * gi + 1] = -1;
     }
+#if !PACK_SIMPLE_D
     if (col_ok) {
       const float z[4] = {0.f, 0.f, 0.f, 0.f};
       VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
       VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
     }
+#endif
     const int pb = gi * P;
     const int pe = min(pb + P, nvalid);
     if (pb < pe) {
@@ -288,6 +303,18 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #pragma unroll
           for (int u = 0; u < U; ++u) prod(q[u].x, pr[u]);
         }
+#if PACK_FASTWIN
+        if (p + U <= nxt) {  // no row starts inside [p, p + U)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float v = __uint_as_float(q[u].y);
+            const f32x2 vv = f2_pack(v, v);
+            acc.lo = f2_fma(vv, pr[u].lo, acc.lo);
+            acc.hi = f2_fma(vv, pr[u].hi, acc.hi);
+          }
+          continue;
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(p + u, __uint_as_float(q[u].y), pr[u]);
       }
@@ -307,6 +334,28 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     }
     __syncthreads();
     // ---------------------------------------------------------------- D
+#if PACK_SIMPLE_D
+    // A row that crosses pieces a..b left a tail entry in piece a and a head
+    // entry in each of a+1..b; its sum is tail(a) + head(a+1) + ... + head(b)
+    // in piece order (the order of the scan-based fold it replaces).
+    {
+      constexpr int RC = (LPG * 4 + 31) / 32;
+      for (int t = warp; t < G; t += kFWarps) {
+        const int row = s_bnd_row[2 * t + 1];
+        if (row < 0) continue;
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+          const int c = q * 32 + lane;
+          if (c < R) {
+            float run = s_bnd[(2 * t + 1) * R + c];
+            for (int j = t + 1; j < G && s_bnd_row[2 * j] == row; ++j) run += s_bnd[(2 * j) * R + c];
+            if (direct) out_rows[row * R + c] = run;
+            else s_acc[row * R + c] += run;
+          }
+        }
+      }
+    }
+#else
     {
       constexpr int E = (2 * G + kFWarps - 1) / kFWarps;
       constexpr int RC = (LPG * 4 + 31) / 32;
@@ -354,6 +403,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         }
       }
     }
+#endif
   }
   if (!direct) {
     __syncthreads();
