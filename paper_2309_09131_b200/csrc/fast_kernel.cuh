@@ -20,6 +20,13 @@
 #ifndef FAST_U
 #define FAST_U 4
 #endif
+// phase D / phase C variants as in pack_kernel.cuh (PACK_SIMPLE_D, PACK_FASTWIN)
+#ifndef FAST_SIMPLE_D
+#define FAST_SIMPLE_D 1
+#endif
+#ifndef FAST_FASTWIN
+#define FAST_FASTWIN 0  // c3 22.20 (off) vs 22.45 ms (on): the 80-register tile kernel loses more than it saves
+#endif
 #ifndef FAST_IPT
 #define FAST_IPT 8
 #endif
@@ -329,11 +336,13 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       s_bnd_row[2 * gi] = -1;
       s_bnd_row[2 * gi + 1] = -1;
     }
+#if !FAST_SIMPLE_D
     if (col_ok) {
       const float z[4] = {0.f, 0.f, 0.f, 0.f};
       VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
       VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
     }
+#endif
     const int pb = gi * P;
 #ifdef FAST_NO_C  // experiment only
     const int pe = pb;
@@ -427,6 +436,15 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #pragma unroll
           for (int u = 0; u < U; ++u) element_prod(fb, q[u], pr[u]);
         }
+#if FAST_FASTWIN
+        if (comp<MODE>(q[U - 1]) == cur) {  // sorted: the whole window is in row cur
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = fmaf(vv[u], pr[u][k], acc[k]);
+          continue;
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
       }
@@ -449,6 +467,27 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     __syncthreads();
     FAST_PROBE(3);
     // ---------------------------------------------------------------- D
+#if FAST_SIMPLE_D
+    // a row crossing pieces a..b: tail(a) + head(a+1) + ... + head(b), in
+    // piece order (see pack_kernel.cuh)
+    {
+      constexpr int RC = (LPG * 4 + 31) / 32;
+      for (int t = warp; t < G; t += kFWarps) {
+        const int row = s_bnd_row[2 * t + 1];
+        if (row < 0) continue;
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+          const int c = q * 32 + lane;
+          if (c < R) {
+            float run = s_bnd[(2 * t + 1) * R + c];
+            for (int j = t + 1; j < G && s_bnd_row[2 * j] == row; ++j) run += s_bnd[(2 * j) * R + c];
+            if (direct) out_rows[row * R + c] = run;
+            else s_acc[row * R + c] += run;
+          }
+        }
+      }
+    }
+#else
     // Boundary entries are in sorted-row order (H0 T0 H1 T1 ...), unused ones
     // hold zeros.  Warp w folds every run of equal rows that *starts* in
     // entries [w * E, (w + 1) * E): find the run's end from the row array,
@@ -500,6 +539,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         }
       }
     }
+#endif
     FAST_PROBE(4);
   }
   if (!direct) {

@@ -33,6 +33,13 @@
 #endif
 // phase D: one warp per tail entry folds the head entries that continue its
 // row (no scans over empty entries, no zeroing of the boundary tiles)
+// phase C reads the sorted tile two records at a time (LDS.128); pieces are
+// padded by 16 B so they start 16-B aligned and the 4 groups of a warp hit
+// different banks.  Needs an even PACK_U.
+#ifndef PACK_PAIRS
+#define PACK_PAIRS 0
+#endif
+#define PACK_PAD (PACK_PAIRS ? 2 : 1)
 #ifndef PACK_SIMPLE_D
 #define PACK_SIMPLE_D 1
 #endif
@@ -43,7 +50,7 @@ template <int LPG>
 struct PackPlan {
   static constexpr int G = kFBlock / LPG;
   static constexpr int P = kFTile / G;
-  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + G);
+  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + PACK_PAD * G);
   static constexpr size_t misc_bytes = 4 * (kFWarps + 4 + G);
   static constexpr size_t fixed_bytes = sorted_bytes + misc_bytes;
   __host__ __device__ static size_t hist_bytes(int64_t m) {
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   const int lg = tid % LPG;
   const int col = lg * 4;
   const bool col_ok = RT > 0 ? true : col < R;
-  auto phys = [](int pos) { return pos + pos / P; };
+  auto phys = [](int pos) { return pos + PACK_PAD * (pos / P); };
   auto key_of = [&](const int4 &r) {
     const int lr = comp<MODE>(r) - irow0;
     return (lr >= 0 && lr < rows) ? lr : -1;
@@ -292,12 +299,22 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         pr.lo = f2_mul(f1.lo, f2.lo);
         pr.hi = f2_mul(f1.hi, f2.hi);
       };
-      const uint2 *sp = s_sorted + gi;  // pad of piece gi
+      const uint2 *sp = s_sorted + PACK_PAD * gi;  // pads of the pieces before gi
       int p = pb;
       for (; p + U <= pe; p += U) {
         uint2 q[U];
+#if PACK_PAIRS
+        static_assert(U % 2 == 0, "PACK_PAIRS needs an even PACK_U");
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+          const uint4 q2 = *reinterpret_cast<const uint4 *>(sp + p + u);
+          q[u] = make_uint2(q2.x, q2.y);
+          q[u + 1] = make_uint2(q2.z, q2.w);
+        }
+#else
 #pragma unroll
         for (int u = 0; u < U; ++u) q[u] = sp[p + u];
+#endif
         f32x4p pr[U];
         if (col_ok) {
 #pragma unroll
