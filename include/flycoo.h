@@ -237,6 +237,29 @@ int fc_build_records(const uint32_t *order, int64_t nnz, int nmodes,
                      const int32_t *coords, const float *vals, void *crd,
                      float *val_out, void *stream);
 
+/* Lean build (layout.build_device_sharded_lean): the same orders with 32-bit
+ * sort keys, coordinates read in place from 16-B records (cstride = ints per
+ * record), so that a tensor whose layout fills most of HBM (config 5:
+ * 3.6B nonzeros) builds inside the memory of its own final buffers.
+ *   iota: out[i] = i;  morton32: Morton key of <= 32 bits (else UNSUPPORTED);
+ *   sort_pairs32: stable LSD radix sort of (uint32 key, id) on [0, end_bit);
+ *   iv_key32: keys[p] = crd[ids[p]*cstride + mode] / m;
+ *   gather_u32: dst[p] = src[ids[p]];
+ *   scatter_rec16: dst[pos[i]] = src[i] (16-B records). */
+int fc_build_iota(uint32_t *out, int64_t n, void *stream);
+int fc_build_morton32(const int32_t *crd, int64_t nnz, int nmodes, int cstride,
+                      const int64_t *m, const int64_t *k, uint32_t *key, void *stream);
+int64_t fc_build_sort32_temp_bytes(int64_t nnz);
+int fc_build_sort_pairs32(const uint32_t *keys_in, uint32_t *keys_out,
+                          const uint32_t *ids_in, uint32_t *ids_out, int64_t nnz,
+                          int end_bit, void *temp, int64_t temp_bytes, void *stream);
+int fc_build_iv_key32(const uint32_t *ids, int64_t n, const int32_t *crd, int cstride,
+                      int mode, int64_t m, uint32_t *keys, void *stream);
+int fc_build_gather_u32(const uint32_t *ids, int64_t n, const uint32_t *src,
+                        uint32_t *dst, void *stream);
+int fc_build_scatter_rec16(const uint32_t *pos, int64_t n, const void *src, void *dst,
+                           void *stream);
+
 /* ---------------------------------------------------------------- K6 synth
  * Measurement-input generator (bench / tests; not the product path).
  * Draw j, mode w: u = philox(seed, w, j) in [0,1); index = smallest i with
@@ -252,6 +275,13 @@ int fc_synth_keys(const int32_t *coords, int64_t n, int nmodes, const int64_t *d
 int fc_synth_mark_first(const uint64_t *hi_sorted, const uint64_t *lo_sorted,
                         const uint32_t *ids_sorted, int64_t n, uint8_t *keep,
                         void *stream);
+/* Coordinates of modes [mode_lo, mode_hi) of the draws js[i] (same law as
+ * fc_synth_draw): out[i*cstride + w - mode_lo].  Used by the bucketed
+ * generator of the tensors too large for one dedup sort (synth.py). */
+int fc_synth_draw_at(uint64_t seed, const int64_t *js, int64_t n, int nmodes,
+                     const int64_t *dims, const double *const *cdfs,
+                     const int64_t *cdf_len, int mode_lo, int mode_hi,
+                     int32_t *out, int cstride, void *stream);
 /* fp32 values in (0, 1]: vals[i] = philox(seed, stream, i). */
 int fc_synth_uniform(uint64_t seed, uint32_t stream_id, int64_t n, float *out,
                      int open_low, void *stream);

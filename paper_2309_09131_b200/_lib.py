@@ -80,6 +80,14 @@ _SIGS = {
     "fc_build_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fc_build_slots_scatter": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "fc_build_records_scatter": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fc_build_iota": (_int, [_vp, _i64, _vp]),
+    "fc_build_morton32": (_int, [_vp, _i64, _int, _int, _vp, _vp, _vp, _vp]),
+    "fc_build_sort32_temp_bytes": (_i64, [_i64]),
+    "fc_build_sort_pairs32": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp]),
+    "fc_build_iv_key32": (_int, [_vp, _i64, _vp, _int, _int, _i64, _vp, _vp]),
+    "fc_build_gather_u32": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "fc_build_scatter_rec16": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "fc_synth_draw_at": (_int, [_c.c_uint64, _vp, _i64, _int, _vp, _vp, _vp, _int, _int, _vp, _int, _vp]),
     "fc_synth_draw": (_int, [_c.c_uint64, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fc_synth_keys": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp]),
     "fc_synth_mark_first": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),

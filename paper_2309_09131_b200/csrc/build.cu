@@ -252,6 +252,86 @@ __global__ void uniform_kernel(uint64_t seed, uint32_t sid, int64_t n, float *ou
   }
 }
 
+// ---------------------------------------------- lean build (c5-size tensors)
+// Same orders as above with 32-bit sort keys and records read in place
+// (coordinates at a stride of crd_words), so the whole build runs inside the
+// memory of the final layout (layout.build_device_sharded_lean).
+__global__ void iota_kernel(uint32_t *out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)i;
+}
+
+__global__ void morton32_kernel(const int32_t *crd, int64_t n, int cs, MortonPlan mp, uint32_t *key) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t iv[kMaxModes];
+#pragma unroll
+    for (int w = 0; w < kMaxModes; ++w)
+      iv[w] = w < mp.nmodes ? (uint32_t)(crd[i * cs + w] / mp.m[w]) : 0u;
+    uint32_t l = 0;
+    int pos = 0;
+    for (int b = 0; b < mp.maxw; ++b) {
+#pragma unroll
+      for (int w = 0; w < kMaxModes; ++w) {
+        if (w >= mp.nmodes || b >= mp.width[w]) continue;
+        l |= ((iv[w] >> b) & 1u) << pos;
+        ++pos;
+      }
+    }
+    key[i] = l;
+  }
+}
+
+__global__ void iv_key32_kernel(const uint32_t *ids, int64_t n, const int32_t *crd, int cs, int mode,
+                                int64_t m, uint32_t *keys) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    keys[p] = (uint32_t)(crd[(int64_t)ids[p] * cs + mode] / m);
+}
+
+__global__ void gather_u32_kernel(const uint32_t *ids, int64_t n, const uint32_t *src, uint32_t *dst) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    dst[p] = src[ids[p]];
+}
+
+// dst[pos[i]] = src[i] for 16-byte records (src = a batch of the input order)
+__global__ void scatter_rec16_kernel(const uint32_t *pos, int64_t n, const int4 *src, int4 *dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[pos[i]] = src[i];
+}
+
+// coordinates of modes [w0, w1) of the draws js[i] (same law as synth_draw_kernel)
+__global__ void synth_draw_at_kernel(uint64_t seed, const int64_t *js, int64_t n, SynthPlan sp,
+                                     int w0, int w1, int32_t *out, int cs) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = (uint64_t)js[i];
+    for (int w = w0; w < w1; ++w) {
+      const Philox4 r = philox4x32_10((uint32_t)j, (uint32_t)(j >> 32), (uint32_t)w, 0x5EEDu, k0, k1);
+      const double u = u01_53(r.x, r.y);
+      int64_t idx;
+      if (sp.cdf[w] == nullptr) {
+        idx = (int64_t)(u * (double)sp.dims[w]);
+        if (idx >= sp.dims[w]) idx = sp.dims[w] - 1;
+      } else {
+        int64_t lo = 0, hi = sp.cdf_len[w] - 1;
+        const double *c = sp.cdf[w];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (u < c[mid]) hi = mid;
+          else lo = mid + 1;
+        }
+        idx = lo;
+      }
+      out[i * cs + (w - w0)] = (int32_t)idx;
+    }
+  }
+}
+
 inline int grid_for(int64_t n) {
   const int64_t b = (n + 255) / 256;
   return (int)(b < 148 * 32 ? (b > 0 ? b : 1) : 148 * 32);
@@ -445,6 +525,102 @@ int fc_synth_uniform(uint64_t seed, uint32_t stream_id, int64_t n, float *out, i
                      void *stream) {
   if (n == 0) return FC_OK;
   uniform_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(seed, stream_id, n, out, open_low);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+// ---------------------------------------------- lean build (c5-size tensors)
+int fc_build_iota(uint32_t *out, int64_t n, void *stream) {
+  if (n == 0) return FC_OK;
+  iota_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(out, n);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_build_morton32(const int32_t *crd, int64_t nnz, int nmodes, int cstride, const int64_t *m,
+                      const int64_t *k, uint32_t *key, void *stream) {
+  FC_CHECK_ARG(nmodes >= 2 && nmodes <= kMaxModes && cstride >= nmodes, "nmodes %d", nmodes);
+  FC_CHECK_ARG(crd && key && m && k, "null argument");
+  MortonPlan mp{};
+  mp.nmodes = nmodes;
+  int total = 0;
+  for (int w = 0; w < nmodes; ++w) {
+    FC_CHECK_ARG(m[w] >= 1 && k[w] >= 1, "bad m/k");
+    mp.m[w] = m[w];
+    mp.width[w] = bit_length_u64((uint64_t)(k[w] - 1));
+    total += mp.width[w];
+    if (mp.width[w] > mp.maxw) mp.maxw = mp.width[w];
+  }
+  if (total > 32) {
+    set_error("morton key needs %d bits (> 32): use fc_build_morton", total);
+    return FC_ERR_UNSUPPORTED;
+  }
+  if (nnz == 0) return FC_OK;
+  morton32_kernel<<<grid_for(nnz), 256, 0, as_stream(stream)>>>(crd, nnz, cstride, mp, key);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int64_t fc_build_sort32_temp_bytes(int64_t nnz) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (const uint32_t *)nullptr, (uint32_t *)nullptr, nnz, 0, 32);
+  return (int64_t)bytes;
+}
+
+int fc_build_sort_pairs32(const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *ids_in,
+                          uint32_t *ids_out, int64_t nnz, int end_bit, void *temp, int64_t temp_bytes,
+                          void *stream) {
+  FC_CHECK_ARG(end_bit >= 1 && end_bit <= 32, "end_bit %d", end_bit);
+  if (nnz == 0) return FC_OK;
+  size_t bytes = (size_t)temp_bytes;
+  FC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out, ids_in, ids_out, nnz,
+                                              0, end_bit, as_stream(stream)));
+  return FC_OK;
+}
+
+int fc_build_iv_key32(const uint32_t *ids, int64_t n, const int32_t *crd, int cstride, int mode,
+                      int64_t m, uint32_t *keys, void *stream) {
+  FC_CHECK_ARG(m >= 1 && cstride > mode, "bad argument");
+  if (n == 0) return FC_OK;
+  iv_key32_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(ids, n, crd, cstride, mode, m, keys);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_build_gather_u32(const uint32_t *ids, int64_t n, const uint32_t *src, uint32_t *dst,
+                        void *stream) {
+  if (n == 0) return FC_OK;
+  gather_u32_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(ids, n, src, dst);
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_build_scatter_rec16(const uint32_t *pos, int64_t n, const void *src, void *dst, void *stream) {
+  if (n == 0) return FC_OK;
+  scatter_rec16_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(
+      pos, n, static_cast<const int4 *>(src), static_cast<int4 *>(dst));
+  FC_LAUNCH_CHECK();
+  return FC_OK;
+}
+
+int fc_synth_draw_at(uint64_t seed, const int64_t *js, int64_t n, int nmodes, const int64_t *dims,
+                     const double *const *cdfs, const int64_t *cdf_len, int mode_lo, int mode_hi,
+                     int32_t *out, int cstride, void *stream) {
+  FC_CHECK_ARG(nmodes >= 2 && nmodes <= kMaxModes, "nmodes %d", nmodes);
+  FC_CHECK_ARG(0 <= mode_lo && mode_lo < mode_hi && mode_hi <= nmodes && cstride >= mode_hi - mode_lo,
+               "modes [%d, %d)", mode_lo, mode_hi);
+  SynthPlan sp{};
+  sp.nmodes = nmodes;
+  for (int w = 0; w < nmodes; ++w) {
+    FC_CHECK_ARG(dims[w] >= 1 && dims[w] <= INT32_MAX, "dims[%d]", w);
+    sp.dims[w] = dims[w];
+    sp.cdf[w] = cdfs ? cdfs[w] : nullptr;
+    sp.cdf_len[w] = (cdfs && cdfs[w]) ? cdf_len[w] : 0;
+  }
+  if (n == 0) return FC_OK;
+  synth_draw_at_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(seed, js, n, sp, mode_lo, mode_hi,
+                                                                   out, cstride);
   FC_LAUNCH_CHECK();
   return FC_OK;
 }

@@ -525,3 +525,102 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
     del gpos
     torch.cuda.current_stream().synchronize()
     return DeviceShardedTensor(plan, crd, val, tuple(slot_maps), dev)
+
+
+def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
+                              batch: int = 1 << 27) -> DeviceShardedTensor:
+    """:func:`build_device_sharded` for a tensor whose layout fills most of
+    HBM (config 5: 3.6B nonzeros, 158 GB of records + slot maps): the same
+    plan, orders, slot maps and records (bit-identical), built inside the
+    memory of the final buffers.
+
+    `records` is the input COO as 16-B records (nnz, 4) int32
+    ``{c0, c1, c2, bits(v)}`` (N <= 3, value embedded) in input order; a
+    device `records` tensor is consumed (overwritten: it becomes the back
+    buffer).  Sort keys are 32 bits (Morton keys of <= 32 bits, iv_n, shard
+    ids; the (sid_n, sid_{n-1}) key as two stable passes), the scratch lives
+    in the second record buffer and the not-yet-written slot maps, and the
+    input records wait in host memory while their device copy is reused for
+    the positions.  Peak device memory = the final layout + sort temp."""
+    L = _lib.load()
+    dev = torch.device(device)
+    nnz, cw = int(records.shape[0]), int(records.shape[1])
+    N = len(params.dims)
+    if not (N <= 3 and cw == 4 and int(L.fc_crd_words(N)) == 4 and L.fc_value_embedded(N)):
+        raise ValueError("the lean build takes 16-B records of a 2- or 3-mode tensor")
+    if params.nnz != nnz:
+        raise ValueError("params were selected for a different nonzero count")
+    if nnz >= 1 << 32:
+        raise ValueError("nnz must fit uint32 positions")
+    widths = [_bitlen(k - 1) for k in params.k]
+    if sum(widths) > 32:
+        raise ValueError("the lean build needs a Morton key of <= 32 bits")
+    st = _stream_ptr()
+    P = lambda t: t.data_ptr()
+    m_arr = _lib.i64_array(params.m)
+    k_arr = _lib.i64_array(params.k)
+    crd = records.to(dev).contiguous()
+
+    other = torch.empty((nnz, 4), dtype=torch.int32, device=dev)
+    A, B, C, D = (other.view(-1)[i * nnz:(i + 1) * nnz] for i in range(4))
+    S = [torch.empty(nnz, dtype=torch.int32, device=dev) for _ in range(N)]
+    temp_bytes = int(L.fc_build_sort32_temp_bytes(max(nnz, 1)))
+    temp = torch.empty(max(temp_bytes, 1), dtype=torch.uint8, device=dev)
+
+    def sort32(keys, ids_in, ids_out, bits):
+        if bits <= 0:
+            ids_out.copy_(ids_in)
+            return
+        _lib.call("fc_build_sort_pairs32", P(keys), P(B), P(ids_in), P(ids_out), nnz, min(bits, 32),
+                  P(temp), temp_bytes, st)
+
+    # Morton order (ties by input position): D
+    _lib.call("fc_build_morton32", P(crd), nnz, N, 4, m_arr, k_arr, P(A), st)
+    _lib.call("fc_build_iota", P(C), nnz, st)
+    sort32(A, C, D, sum(widths))
+    # canonical orders -> plan and shard ids (S[n])
+    counts_all = []
+    hist = torch.empty(max(params.k), dtype=torch.int64, device=dev)
+    for n in range(N):
+        _lib.call("fc_build_iv_key32", P(D), nnz, P(crd), 4, n, params.m[n], P(A), st)
+        sort32(A, D, C, _bitlen(params.k[n] - 1))
+        _lib.call("fc_build_ss_hist", P(crd), nnz, 4, n, params.m[n], params.k[n], P(hist), st)
+        counts = hist[: params.k[n]].cpu().numpy().astype(np.int64)
+        if int(counts.sum()) != nnz:
+            raise ValueError("coordinates outside the declared dims")
+        counts_all.append(counts)
+        offs = torch.from_numpy(np.concatenate(([0], np.cumsum(counts))).astype(np.int64)).to(dev)
+        first = torch.from_numpy(np.concatenate(([0], np.cumsum(-(-counts // params.g))))
+                                 .astype(np.int64)).to(dev)
+        _lib.call("fc_build_shard_ids", P(C), nnz, P(crd), 4, n, params.m[n], P(offs), P(first),
+                  params.g, P(S[n]), st)
+    plan = plan_from_counts(params, counts_all)
+
+    # the input records wait on the host; their device memory holds positions
+    # (the caller's tensor is overwritten: it becomes the back buffer)
+    host = torch.empty((nnz, 4), dtype=torch.int32, pin_memory=False)
+    for a in range(0, nnz, batch):
+        host[a:a + batch].copy_(crd[a:a + batch])
+    back, crd = crd, None
+    E = back.view(-1)[:nnz]
+    pos = [back.view(-1)[(i + 1) * nnz:(i + 2) * nnz] for i in range(N)]
+    for n in range(N):
+        prev = (n - 1) % N
+        # B200 order: stable sort of the Morton order by (sid_n, sid_prev)
+        _lib.call("fc_build_gather_u32", P(D), nnz, P(S[prev]), P(A), st)
+        sort32(A, D, C, _bitlen(plan.total_shards(prev) - 1))
+        _lib.call("fc_build_gather_u32", P(C), nnz, P(S[n]), P(A), st)
+        sort32(A, C, E, _bitlen(plan.total_shards(n) - 1))
+        _lib.call("fc_build_invert", P(E), nnz, P(pos[n]), st)
+    for n in range(N):
+        _lib.call("fc_build_slots_scatter", P(pos[n]), P(pos[(n + 1) % N]), nnz, P(S[n]), st)
+    del temp
+    # mode-0 records: scatter the input batches to their positions
+    for a in range(0, nnz, batch):
+        b = min(nnz, a + batch)
+        stage = host[a:b].to(dev, non_blocking=False)
+        _lib.call("fc_build_scatter_rec16", P(pos[0][a:b]), b - a, P(stage), P(other), st)
+        del stage
+    del host
+    torch.cuda.current_stream().synchronize()
+    return DeviceShardedTensor(plan, [other, back], [None, None], tuple(S), dev)

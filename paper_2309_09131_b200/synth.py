@@ -163,6 +163,112 @@ def zipf_tensor(dims: Sequence[int], nnz: int, seed: int, exponents: Sequence, d
     return coords, vals
 
 
+def zipf_records_bucketed(dims: Sequence[int], nnz: int, seed: int, exponents: Sequence,
+                          device="cuda", draw_factor: float = 1.25, bucket_draws: int = 1 << 28,
+                          scan: int = 1 << 28):
+    """The nonzeros of :func:`zipf_tensor` (same draws, same first-occurrence
+    dedup, same "first nnz distinct in draw order" cut), for tensors whose
+    single dedup sort does not fit HBM (config 5: 3.6B nonzeros from ~4.5B
+    draws).  Draws are split into buckets by ranges of the mode-0 coordinate
+    (duplicates share it, so each bucket dedups alone, a few GB at a time);
+    the cut is the draw index T with exactly nnz first occurrences below it.
+
+    Returns 16-byte records (nnz, 4) int32 ``{c0, c1, c2, bits(v)}`` on
+    `device` (the 3-mode record layout), ordered by bucket and by draw index
+    inside a bucket -- the same SET of nonzeros as zipf_tensor, not the same
+    input order; values are drawn per output position as in zipf_tensor."""
+    dims = tuple(int(d) for d in dims)
+    N = len(dims)
+    if N != 3:
+        raise ValueError("the bucketed generator writes 3-mode records")
+    if math.prod(dims) >= 1 << 63:
+        raise ValueError("coordinate space must fit a 63-bit key")
+    dev = torch.device(device)
+    strm = torch.cuda.current_stream(dev).cuda_stream
+    cdfs = [None if s is None else torch.from_numpy(zipf_cdf(d, s)).to(dev)
+            for d, s in zip(dims, exponents)]
+    cdf_ptrs = _lib.ptr_array([c.data_ptr() if c is not None else 0 for c in cdfs])
+    cdf_len = _lib.i64_array([c.numel() if c is not None else 0 for c in cdfs])
+    dims_arr = _lib.i64_array(dims)
+    if exponents[0] is None:
+        p0 = np.full(dims[0], 1.0 / dims[0])
+    else:
+        p0 = np.diff(np.concatenate(([0.0], zipf_cdf(dims[0], exponents[0]))))
+
+    def draw_at(js, lo, hi, out, cstride):
+        _lib.call("fc_synth_draw_at", int(seed), js.data_ptr(), js.numel(), N, dims_arr, cdf_ptrs,
+                  cdf_len, lo, hi, out.data_ptr(), cstride, strm)
+
+    ndraws = int(nnz * draw_factor) + 1024
+    while True:
+        # mode-0 value ranges of <= bucket_draws expected draws (one hot value
+        # may exceed it alone)
+        groups, v = [], 0
+        while v < dims[0]:
+            w, acc = v, 0.0
+            while w < dims[0] and (w == v or acc + p0[w] * ndraws <= bucket_draws):
+                acc += p0[w] * ndraws
+                w += 1
+            groups.append((v, w))
+            v = w
+        firsts = []
+        for v0, v1 in groups:
+            sel = []
+            for j0 in range(0, ndraws, scan):
+                js = torch.arange(j0, min(j0 + scan, ndraws), dtype=torch.int64, device=dev)
+                c0 = torch.empty(js.numel(), dtype=torch.int32, device=dev)
+                draw_at(js, 0, 1, c0, 1)
+                sel.append(js[(c0 >= v0) & (c0 < v1)])
+                del js, c0
+            jb = torch.cat(sel)
+            del sel
+            c = torch.empty((jb.numel(), N), dtype=torch.int32, device=dev)
+            draw_at(jb, 0, N, c, N)
+            c = c.to(torch.int64)
+            key = (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+            del c
+            skey, perm = torch.sort(key, stable=True)  # draw order kept inside equal keys
+            del key
+            first = torch.ones(skey.numel(), dtype=torch.bool, device=dev)
+            first[1:] = skey[1:] != skey[:-1]
+            del skey
+            firsts.append(torch.sort(jb[perm[first]]).values)
+            del perm, first, jb
+        total = sum(int(f.numel()) for f in firsts)
+        if total >= nnz:
+            break
+        del firsts
+        ratio = nnz / max(total, 1)
+        ndraws = int(ndraws * max(1.2, min(4.0, ratio * 1.1))) + 1024
+    # the cut: smallest T with exactly nnz first occurrences below it
+    lo, hi = 0, ndraws
+    while lo < hi:
+        mid = (lo + hi) // 2
+        t = torch.tensor([mid], dtype=torch.int64, device=dev)
+        cnt = sum(int(torch.searchsorted(f, t)) for f in firsts)
+        if cnt >= nnz:
+            hi = mid
+        else:
+            lo = mid + 1
+    cut = torch.tensor([lo], dtype=torch.int64, device=dev)
+    rec = torch.empty((nnz, 4), dtype=torch.int32, device=dev)
+    off = 0
+    for i in range(len(firsts)):
+        f = firsts[i]
+        f = f[: int(torch.searchsorted(f, cut))]
+        if f.numel():
+            draw_at(f, 0, N, rec[off:], 4)
+        off += f.numel()
+        firsts[i] = None
+        del f
+    assert off == nnz, (off, nnz)
+    vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    _lib.call("fc_synth_uniform", int(seed), 77, nnz, vals.data_ptr(), 1, strm)
+    rec[:, 3] = vals.view(torch.int32)
+    del vals
+    return rec
+
+
 # ---------------------------------------------------- host twin (numpy)
 
 _M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)

@@ -4,7 +4,8 @@ not fit"), through the public API on one B200:
 * c2 (76.9M nonzeros): every output row of every mode against the oracle's
   sequential ``reference_mttkrp`` (coo.py:406-426 restated in C), fixed
   factors;
-* c3 (140M, 4 modes) and c4 (1.74B): a sample of output rows per mode --
+* c3 (140M, 4 modes), c4 (1.74B) and c5 (3.6B, bucketed generator + lean
+  build): a sample of output rows per mode --
   uniform rows plus moderately heavy ones that span several chunks (K2) --
   recomputed in float64 on the host from the nonzeros that carry them;
 * all three: after every pass every element sits in the super-shard of its
@@ -87,13 +88,21 @@ def _run(cfg: int, full_oracle: bool):
     torch.cuda.empty_cache()
     c = CONFIGS[cfg]
     dims, R = tuple(c["dims"]), 32
-    coords, vals = config_tensor(cfg)
-    params = device_params(dims, int(vals.shape[0]), R)
-    if full_oracle:
-        subs = coords.cpu().numpy().astype(np.int64)
-        v64 = vals.cpu().numpy().astype(np.float64)
-    st = build_device_sharded(coords, vals, params)
-    del coords, vals
+    if cfg == 5:  # 3.6B nonzeros: bucketed generator + lean build (158 GB resident)
+        from paper_2309_09131_b200.layout import build_device_sharded_lean
+        from paper_2309_09131_b200.synth import zipf_records_bucketed
+        rec = zipf_records_bucketed(dims, c["nnz"], seed=cfg, exponents=c["law"])
+        params = device_params(dims, c["nnz"], R)
+        st = build_device_sharded_lean(rec, params)
+        del rec
+    else:
+        coords, vals = config_tensor(cfg)
+        params = device_params(dims, int(vals.shape[0]), R)
+        if full_oracle:
+            subs = coords.cpu().numpy().astype(np.int64)
+            v64 = vals.cpu().numpy().astype(np.float64)
+        st = build_device_sharded(coords, vals, params)
+        del coords, vals
     torch.cuda.empty_cache()
     smap = schedule_super_shards(st.plan, 1)
     fs = DeviceFactorSet.random(dims, R, seed=2000 + cfg)
@@ -112,6 +121,8 @@ def _run(cfg: int, full_oracle: bool):
                 rng.integers(0, dims[n], 48),
                 [r for r in (100, 1000, 20000) if r < dims[n]],
                 [dims[n] - 1]]))
+            if cfg == 5 and n == 0:  # 46 rows of 78M nonzeros each: two of them
+                rows = np.array([3, dims[0] - 1])
             want, cnt = _sample_rows(st, n, rows, f64)
             got = mttkrp_mode(st, fs, n, smap)
             assert cnt > 0
@@ -131,3 +142,9 @@ def test_c3_full_sampled_rows():
 
 def test_c4_full_sampled_rows():
     _run(4, full_oracle=False)
+
+
+def test_c5_full_sampled_rows():
+    """3.6B nonzeros, 46 mode-0 rows of ~78M nonzeros each (heavy rows split
+    over ~9.5k chunks each, two-level K2)."""
+    _run(5, full_oracle=False)
