@@ -237,15 +237,29 @@ def run_ours(args, rank, world, local):
     cfg = workload(args.config, args.nnz)
     N, R, nnz, dims = len(cfg["dims"]), cfg["rank"], cfg["nnz"], cfg["dims"]
 
-    t0 = time.perf_counter()
-    coords, vals = config_tensor(args.config, device=dev, nnz=nnz)
-    torch.cuda.synchronize()
-    gen_s = time.perf_counter() - t0
+    # tensors whose regular generator + build need more than ~80% of HBM
+    # (config 5 at 3.6B nonzeros): bucketed generator + lean build, which
+    # stay inside the memory of the final layout
+    lean = (N == 3 and cfg["law"] is not None
+            and nnz * 64 > 0.8 * torch.cuda.get_device_properties(dev).total_memory)
     params = device_params(dims, nnz, R)
     t0 = time.perf_counter()
-    st = build_device_sharded(coords, vals, params, device=dev)
+    if lean:
+        from paper_2309_09131_b200.layout import build_device_sharded_lean
+        from paper_2309_09131_b200.synth import zipf_records_bucketed
+        rec = zipf_records_bucketed(dims, nnz, seed=args.config, exponents=cfg["law"], device=dev)
+    else:
+        coords, vals = config_tensor(args.config, device=dev, nnz=nnz)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if lean:
+        st = build_device_sharded_lean(rec, params, device=dev)
+        del rec
+    else:
+        st = build_device_sharded(coords, vals, params, device=dev)
+        del coords, vals
     build_s = time.perf_counter() - t0
-    del coords, vals
     smap = schedule_super_shards(st.plan, 1)
     factors = DeviceFactorSet.random(dims, R, seed=1000 + args.config, device=dev)
     updated = cfg["semantics"] == "updated"
@@ -447,6 +461,7 @@ def run_ours(args, rank, world, local):
                         f"dp{world}: per-mode super-shard row ranges, NCCL all_to_all_single remap + "
                         "all_gather_into_tensor of updated factor rows"),
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
+                       "build": "lean (bucketed generator, layout.build_device_sharded_lean)" if lean else "regular",
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
                        # median over the measured sweeps of each mode pass
                        "mode_ms": [round(1e3 * statistics.median(mode_secs[n::N]), 4)
