@@ -40,6 +40,14 @@
 #define PACK_PAIRS 0
 #endif
 #define PACK_PAD (PACK_PAIRS ? 2 : 1)
+// phase A without per-item bounds tests on full tiles
+#ifndef PACK_FULL_TILE
+#define PACK_FULL_TILE 1
+#endif
+// cheaper ballot rounds (no per-bit guard, no select)
+#ifndef PACK_BALLOT2
+#define PACK_BALLOT2 1
+#endif
 #ifndef PACK_SIMPLE_D
 #define PACK_SIMPLE_D 1
 #endif
@@ -130,27 +138,44 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     // ---------------------------------------------------------------- A
     int4 rec[kFIPT];
     uint32_t slot[kFIPT];
+#if PACK_FULL_TILE
+    if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
-    for (int j = 0; j < kFIPT; ++j) {
-      const int e = j * kFBlock + tid;
-      if (e < cnt) {
-        const int64_t i = t0 + e;
+      for (int j = 0; j < kFIPT; ++j) {
+        const int64_t i = t0 + j * kFBlock + tid;
         rec[j] = ld_stream_v4(a.src + i);
         if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
-      } else {
-        rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
+      }
+    } else
+#endif
+    {
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        const int e = j * kFBlock + tid;
+        if (e < cnt) {
+          const int64_t i = t0 + e;
+          rec[j] = ld_stream_v4(a.src + i);
+          if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
+        } else {
+          rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
+        }
       }
     }
     for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int e = j * kFBlock + tid;
-      if (e < cnt) {
+      if (PACK_FULL_TILE ? (cnt == kFTile || e < cnt) : e < cnt) {
         if (a.do_remap) {
           remap_store<1, true, PEER>(a, slot[j], rec[j], rec[j], 0.f);
         }
-        if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
       }
+    }
+    {  // a record outside the chunk's super-shard rows (invalid items: -1 by design)
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) bad |= (j * kFBlock + tid < cnt) && key_of(rec[j]) < 0;
+      if (bad) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
     }
     __syncwarp();
     // ---------------------------------------------------------------- B
@@ -166,6 +191,22 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #if PACK_BALLOT_MATCH
       // equal-row peers from one ballot per key bit (rows < 2^hbits)
       unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
+#if PACK_BALLOT2
+      // bits >= hbits are 0 for every valid lane, so extra rounds only drop
+      // invalid lanes again: 6 fixed rounds for <= 64 rows, else 8
+      auto round = [&](int b) {
+        const unsigned bit = ((unsigned)k >> b) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= m ^ (bit - 1u);  // m if the bit is set, ~m if not
+      };
+      if (hbits <= 6) {
+#pragma unroll
+        for (int b = 0; b < 6; ++b) round(b);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) round(b);
+      }
+#else
 #pragma unroll
       for (int b = 0; b < 8; ++b) {  // rows <= 256; the guard is warp-uniform
         if (b < hbits) {
@@ -174,6 +215,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
           peers &= bit ? m : ~m;
         }
       }
+#endif
       const unsigned grp = k >= 0 ? peers : (1u << lane);
 #else
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
