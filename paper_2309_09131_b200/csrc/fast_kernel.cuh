@@ -27,6 +27,12 @@
 #ifndef FAST_FASTWIN
 #define FAST_FASTWIN 0  // c3 22.20 (off) vs 22.45 ms (on): the 80-register tile kernel loses more than it saves
 #endif
+#ifndef FAST_FULL_TILE
+#define FAST_FULL_TILE 1
+#endif
+#ifndef FAST_BALLOT_MATCH
+#define FAST_BALLOT_MATCH 1
+#endif
 #ifndef FAST_IPT
 #define FAST_IPT 8
 #endif
@@ -157,6 +163,9 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
+#if FAST_BALLOT_MATCH
+  const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
+#endif
   int4 *s_sorted = reinterpret_cast<int4 *>(smem);
   float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
   int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
@@ -218,16 +227,29 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     int4 rec[kFIPT];
     float rv[kFIPT];
     uint32_t slot[kFIPT];
+#if FAST_FULL_TILE
+    if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
-    for (int j = 0; j < kFIPT; ++j) {
-      const int e = j * kFBlock + tid;
-      if (e < cnt) {
-        const int64_t i = t0 + e;
+      for (int j = 0; j < kFIPT; ++j) {
+        const int64_t i = t0 + j * kFBlock + tid;
         rec[j] = ld_stream_v4(a.src + i);
         if (!EMB) rv[j] = ld_stream_f32(a.src_val + i);
         if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
-      } else {
-        rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
+      }
+    } else
+#endif
+    {
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        const int e = j * kFBlock + tid;
+        if (e < cnt) {
+          const int64_t i = t0 + e;
+          rec[j] = ld_stream_v4(a.src + i);
+          if (!EMB) rv[j] = ld_stream_f32(a.src_val + i);
+          if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
+        } else {
+          rec[j] = make_int4(INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN);
+        }
       }
     }
     for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
@@ -263,7 +285,25 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
+#if FAST_BALLOT_MATCH
+      // equal-row peers from one ballot per key bit (pack_kernel.cuh)
+      unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
+      auto round = [&](int b) {
+        const unsigned bit = ((unsigned)k >> b) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= m ^ (bit - 1u);
+      };
+      if (hbits <= 6) {
+#pragma unroll
+        for (int b = 0; b < 6; ++b) round(b);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) round(b);
+      }
+      const unsigned grp = k >= 0 ? peers : (1u << lane);
+#else
       const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
+#endif
       // the group leader reserves the run (a warp's shared atomics to one
       // address execute in issue order: stable) and broadcasts its base
       const int leader = __ffs(grp) - 1;
