@@ -48,7 +48,7 @@ __all__ = ["PeerModePlan", "partition_chunks", "super_shard_owners", "peer_plans
 @dataclass
 class PeerModePlan:
     """One GPU's share of one mode pass.  GPUs take contiguous ranges of the
-    single-GPU chunk list (balanced by nonzeros), so a heavy super-shard's
+    single-GPU chunk list (balanced by nonzeros + a per-chunk cost), so a heavy super-shard's
     chunks may run on several GPUs; its rows stay owned by ONE GPU (the one
     running its first chunk), which reduces all its partial tiles."""
     c_lo: int                   # chunk range [c_lo, c_hi) of the global plan
@@ -69,15 +69,24 @@ class PeerModePlan:
         return self.e_hi - self.e_lo
 
 
-def partition_chunks(chunk_start: np.ndarray, world: int) -> np.ndarray:
+# Cost of one chunk beyond its nonzeros, in nonzero equivalents: a chunk pays
+# its tile passes' fixed work (barriers, histogram scan, boundary fold) and its
+# accumulator tile however few nonzeros it holds, so a GPU whose range is the
+# Zipf tail (many small super-shards) is slower than its nonzero share says.
+CHUNK_WEIGHT = int(os.environ.get("FLYCOO_CHUNK_WEIGHT", "4096"))
+
+
+def partition_chunks(chunk_start: np.ndarray, world: int, chunk_weight: int | None = None) -> np.ndarray:
     """world + 1 chunk bounds splitting the chunk list into contiguous ranges
-    of ~equal nonzero counts."""
+    of ~equal cost = nonzeros + chunk_weight per chunk."""
     nch = chunk_start.shape[0] - 1
-    total = int(chunk_start[-1] - chunk_start[0])
+    kw = CHUNK_WEIGHT if chunk_weight is None else int(chunk_weight)
+    # cost before chunk c (c = 0..nch)
+    cost = (chunk_start - chunk_start[0]).astype(np.float64) + kw * np.arange(nch + 1, dtype=np.float64)
+    total = cost[-1]
     cb = [0]
     for p in range(1, world):
-        target = chunk_start[0] + p * total / world
-        c = int(np.searchsorted(chunk_start[:nch], target, side="left"))
+        c = int(np.searchsorted(cost[:nch], p * total / world, side="left"))
         cb.append(min(max(c, cb[-1]), nch))
     cb.append(nch)
     return np.asarray(cb, dtype=np.int64)

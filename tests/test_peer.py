@@ -125,11 +125,19 @@ def test_chunk_partition_balances_a_heavy_super_shard():
     w = make_mode_work(plan, 0, 8, "cpu", chunk_elems=2048)
     cs = w.chunk_start.numpy()
     for world in (2, 4, 8):
-        cb = partition_chunks(cs, world)
-        loads = np.diff(cs[cb])
+        # pure nonzero balance (chunk_weight 0): within one chunk of the ideal
+        loads = np.diff(cs[partition_chunks(cs, world, chunk_weight=0)])
         assert loads.max() <= len(subs) / world + 2048, (world, loads)
+        # default: nonzeros + a fixed cost per chunk, balanced within one chunk's cost
+        cb = partition_chunks(cs, world)
+        nch = len(cs) - 1
+        kw = 4096
+        costs = np.diff(cs[cb]) + kw * np.diff(cb)
+        assert costs.max() <= (len(subs) + kw * nch) / world + 2048 + kw, (world, costs)
         gpu = np.repeat(np.arange(world), np.diff(cb))
         owner = super_shard_owners(w, params.k[0], 64, gpu, world)
         assert owner[0] == 0 and np.all(np.diff(owner) >= 0)
-        # the heavy super-shard's chunks run on several GPUs
-        assert len(set(gpu[w.chunk_ss.numpy() == 0])) > 1
+        # the heavy super-shard's chunks run on several GPUs once it holds more
+        # than one GPU's share of the cost (at world 2 the cut may land on its end)
+        if world >= 4:
+            assert len(set(gpu[w.chunk_ss.numpy() == 0])) > 1

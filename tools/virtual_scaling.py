@@ -8,7 +8,9 @@ sweep from below (NVLink transfer and barriers not included).  The same is
 reported for the super-shard partition (rows never split; dist.py), to show
 what splitting the Zipf head super-shard buys.
 
-usage: python tools/virtual_scaling.py [config]   (default 2)
+usage: python tools/virtual_scaling.py [config [nnz]]   (default 2; nnz overrides the size --
+the P ranks' own buffers sit next to the global layout, so the billion-nonzero configs run at a
+reduced size of the same law)
 """
 import json
 import sys
@@ -38,10 +40,11 @@ def timed(fn, reps=5):
 
 def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    nnz = int(sys.argv[2]) if len(sys.argv) > 2 else None
     dev = torch.device("cuda", 0)
     c = CONFIGS[cfg]
     dims, R = tuple(c["dims"]), 32
-    coords, vals = config_tensor(cfg, device=dev)
+    coords, vals = config_tensor(cfg, device=dev, nnz=nnz)
     params = device_params(dims, int(vals.shape[0]), R)
     st = build_device_sharded(coords, vals, params, device=dev)
     del coords, vals
@@ -82,7 +85,8 @@ def main():
         print(P, result["modes"][P], flush=True)
         del ranks
         torch.cuda.empty_cache()
-    out = Path(__file__).resolve().parents[1] / "profiles" / f"r1_virtual_scaling_c{cfg}.json"
+    tag = f"c{cfg}" if nnz is None else f"c{cfg}_nnz{nnz}"
+    out = Path(__file__).resolve().parents[1] / "profiles" / f"r1_virtual_scaling_{tag}.json"
     out.write_text(json.dumps(result, indent=1))
 
 
