@@ -101,6 +101,13 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+#ifdef FAST_PHASE_TIMING
+  unsigned long long ph_acc[5] = {0, 0, 0, 0, 0};
+  long long ph_t = clock64();
+#define PACK_PROBE(k) do { if (tid == 0) { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } } while (0)
+#else
+#define PACK_PROBE(k) do { } while (0)
+#endif
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t chunk = blockIdx.x;
   const int64_t start = a.chunk_start[chunk];
@@ -227,6 +234,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
+    PACK_PROBE(0);
     {
       int tot = 0;
       if (tid < rows) {
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
+    PACK_PROBE(1);
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int x = comp<MODE>(rec[j]);
@@ -274,6 +283,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
+    PACK_PROBE(2);
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
     if (tid == 0 && t0 + kFTile < end) {
@@ -392,6 +402,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
+    PACK_PROBE(3);
     // ---------------------------------------------------------------- D
 #if PACK_SIMPLE_D
     // A row that crosses pieces a..b left a tail entry in piece a and a head
@@ -464,6 +475,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     }
 #endif
   }
+  PACK_PROBE(4);
   if (!direct) {
     __syncthreads();
     float *dstp = part < 0 ? out_rows : partial_ws(a, chunk) + (int64_t)part * a.m * R;
@@ -473,6 +485,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
   }
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
+#ifdef FAST_PHASE_TIMING
+  if (tid == 0)
+    for (int k = 0; k < 5; ++k) atomicAdd(&g_phase_cycles[k], ph_acc[k]);
+#endif
 }
 
 template <int MODE, int LPG, int RT, bool PEER = false>

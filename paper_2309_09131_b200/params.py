@@ -246,16 +246,33 @@ def _explain(dims, model: _Model, gs) -> str:
     return "no feasible (m, g): " + "; ".join(parts)
 
 
-def device_params(dims: Sequence[int], nnz: int, rank: int, acc_tile_bytes: int = 8192,
+def _auto_rows(dim: int, nnz: int, rank: int) -> int:
+    """Super-shard height of one mode (measured on c2-c4, profiles/r1_kernel_experiments.md):
+    a 4 KB accumulator tile when super-shards stay large (>= 64k nonzeros: fewer rows per
+    2048-element tile -> fewer segments, fewer ballot rounds) or become so sparse that
+    <= 4k nonzeros share an 8 KB tile's rows (direct chunks: rows complete inside one tile);
+    8 KB otherwise (fewer, fuller chunks)."""
+    small = max(1, 4096 // (4 * int(rank)))
+    big = max(1, 8192 // (4 * int(rank)))
+    a_small = nnz * small / max(dim, 1)
+    a_big = nnz * big / max(dim, 1)
+    return min(dim, small if (a_small >= 65536 or a_big <= 4096) else big)
+
+
+def device_params(dims: Sequence[int], nnz: int, rank: int, acc_tile_bytes: int | None = None,
                   g: int = 32768, m: Sequence[int] | None = None) -> PartitionParams:
-    """B200 partition: per mode m = acc_tile_bytes / (4 R) rows (one
-    super-shard's fp32 accumulator tile in shared memory), k = ceil(I / m).
+    """B200 partition: per mode m rows per super-shard (one fp32 accumulator
+    tile of m x R in shared memory) -- acc_tile_bytes / (4 R) when given,
+    else chosen per mode by :func:`_auto_rows` -- and k = ceil(I / m).
     gamma/theta/nu are recorded for the cache model only (nu = 1: CTAs,
     not threads, consume super-shards)."""
     dims = tuple(int(d) for d in dims)
     if m is None:
-        width = max(1, acc_tile_bytes // (4 * int(rank)))
-        m = tuple(min(d, width) for d in dims)
+        if acc_tile_bytes is None:
+            m = tuple(_auto_rows(d, nnz, rank) for d in dims)
+        else:
+            width = max(1, int(acc_tile_bytes) // (4 * int(rank)))
+            m = tuple(min(d, width) for d in dims)
     m = tuple(int(x) for x in m)
     k = tuple(_cdiv(d, mm) for d, mm in zip(dims, m))
     rec = 4 * len(dims) + 4
