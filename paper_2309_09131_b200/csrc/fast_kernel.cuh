@@ -293,7 +293,10 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         const unsigned m = __ballot_sync(0xffffffffu, bit);
         peers &= m ^ (bit - 1u);
       };
-      if (hbits <= 6) {
+      if (hbits <= 5) {
+#pragma unroll
+        for (int b = 0; b < 5; ++b) round(b);
+      } else if (hbits <= 6) {
 #pragma unroll
         for (int b = 0; b < 6; ++b) round(b);
       } else {

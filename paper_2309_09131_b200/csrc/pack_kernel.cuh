@@ -200,13 +200,16 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
 #if PACK_BALLOT2
       // bits >= hbits are 0 for every valid lane, so extra rounds only drop
-      // invalid lanes again: 6 fixed rounds for <= 64 rows, else 8
+      // invalid lanes again: 5 fixed rounds for <= 32 rows, 6 for <= 64, else 8
       auto round = [&](int b) {
         const unsigned bit = ((unsigned)k >> b) & 1u;
         const unsigned m = __ballot_sync(0xffffffffu, bit);
         peers &= m ^ (bit - 1u);  // m if the bit is set, ~m if not
       };
-      if (hbits <= 6) {
+      if (hbits <= 5) {
+#pragma unroll
+        for (int b = 0; b < 5; ++b) round(b);
+      } else if (hbits <= 6) {
 #pragma unroll
         for (int b = 0; b < 6; ++b) round(b);
       } else {
