@@ -20,19 +20,6 @@
 #ifndef FAST_U
 #define FAST_U 4
 #endif
-// phase D / phase C variants as in pack_kernel.cuh (PACK_SIMPLE_D, PACK_FASTWIN)
-#ifndef FAST_SIMPLE_D
-#define FAST_SIMPLE_D 1
-#endif
-#ifndef FAST_FASTWIN
-#define FAST_FASTWIN 0  // c3 22.20 (off) vs 22.45 ms (on): the 80-register tile kernel loses more than it saves
-#endif
-#ifndef FAST_FULL_TILE
-#define FAST_FULL_TILE 1
-#endif
-#ifndef FAST_BALLOT_MATCH
-#define FAST_BALLOT_MATCH 1
-#endif
 #ifndef FAST_IPT
 #define FAST_IPT 8
 #endif
@@ -163,9 +150,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
-#if FAST_BALLOT_MATCH
   const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
-#endif
   int4 *s_sorted = reinterpret_cast<int4 *>(smem);
   float *s_sval = reinterpret_cast<float *>(smem + FP::sorted_bytes);
   int *s_misc = reinterpret_cast<int *>(smem + FP::sorted_bytes + FP::sval_bytes);
@@ -227,7 +212,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     int4 rec[kFIPT];
     float rv[kFIPT];
     uint32_t slot[kFIPT];
-#if FAST_FULL_TILE
     if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -237,7 +221,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
       }
     } else
-#endif
     {
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -285,7 +268,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
-#if FAST_BALLOT_MATCH
       // equal-row peers from one ballot per key bit (pack_kernel.cuh)
       unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
       auto round = [&](int b) {
@@ -293,10 +275,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         const unsigned m = __ballot_sync(0xffffffffu, bit);
         peers &= m ^ (bit - 1u);
       };
-      if (hbits <= 5) {
-#pragma unroll
-        for (int b = 0; b < 5; ++b) round(b);
-      } else if (hbits <= 6) {
+      if (hbits <= 6) {
 #pragma unroll
         for (int b = 0; b < 6; ++b) round(b);
       } else {
@@ -304,9 +283,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         for (int b = 0; b < 8; ++b) round(b);
       }
       const unsigned grp = k >= 0 ? peers : (1u << lane);
-#else
-      const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
-#endif
       // the group leader reserves the run (a warp's shared atomics to one
       // address execute in issue order: stable) and broadcasts its base
       const int leader = __ffs(grp) - 1;
@@ -379,13 +355,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       s_bnd_row[2 * gi] = -1;
       s_bnd_row[2 * gi + 1] = -1;
     }
-#if !FAST_SIMPLE_D
-    if (col_ok) {
-      const float z[4] = {0.f, 0.f, 0.f, 0.f};
-      VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
-      VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
-    }
-#endif
     const int pb = gi * P;
 #ifdef FAST_NO_C  // experiment only
     const int pe = pb;
@@ -479,15 +448,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #pragma unroll
           for (int u = 0; u < U; ++u) element_prod(fb, q[u], pr[u]);
         }
-#if FAST_FASTWIN
-        if (comp<MODE>(q[U - 1]) == cur) {  // sorted: the whole window is in row cur
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] = fmaf(vv[u], pr[u][k], acc[k]);
-          continue;
-        }
-#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
       }
@@ -510,7 +470,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     __syncthreads();
     FAST_PROBE(3);
     // ---------------------------------------------------------------- D
-#if FAST_SIMPLE_D
     // a row crossing pieces a..b: tail(a) + head(a+1) + ... + head(b), in
     // piece order (see pack_kernel.cuh)
     {
@@ -530,59 +489,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         }
       }
     }
-#else
-    // Boundary entries are in sorted-row order (H0 T0 H1 T1 ...), unused ones
-    // hold zeros.  Warp w folds every run of equal rows that *starts* in
-    // entries [w * E, (w + 1) * E): find the run's end from the row array,
-    // then sum its entries in entry order with independent loads.
-    {
-      constexpr int E = (2 * G + kFWarps - 1) / kFWarps;
-      constexpr int RC = (LPG * 4 + 31) / 32;
-      const int ent0 = warp * E;
-      const int ent_end = min(2 * G, ent0 + E);
-      int prev = -1;
-      for (int e2 = ent0 - 1; e2 >= 0; --e2) {
-        const int r2 = s_bnd_row[e2];
-        if (r2 >= 0) {
-          prev = r2;
-          break;
-        }
-      }
-      for (int ent = ent0; ent < ent_end; ++ent) {
-        const int row = s_bnd_row[ent];
-        if (row < 0 || row == prev) {
-          if (row >= 0) prev = row;
-          continue;
-        }
-        prev = row;
-        int e3 = ent + 1;
-        while (e3 < 2 * G) {
-          const int r3 = s_bnd_row[e3];
-          if (r3 >= 0 && r3 != row) break;
-          ++e3;
-        }
-#pragma unroll
-        for (int q = 0; q < RC; ++q) {
-          const int c = q * 32 + lane;
-          if (c < R) {
-            float run = 0.f;
-            int e = ent;
-            for (; e + 4 <= e3; e += 4) {
-              const float x0 = s_bnd[e * R + c], x1 = s_bnd[(e + 1) * R + c];
-              const float x2 = s_bnd[(e + 2) * R + c], x3 = s_bnd[(e + 3) * R + c];
-              run += x0;
-              run += x1;
-              run += x2;
-              run += x3;
-            }
-            for (; e < e3; ++e) run += s_bnd[e * R + c];
-            if (direct) out_rows[row * R + c] = run;
-            else s_acc[row * R + c] += run;
-          }
-        }
-      }
-    }
-#endif
     FAST_PROBE(4);
   }
   if (!direct) {

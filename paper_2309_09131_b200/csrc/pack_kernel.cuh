@@ -21,36 +21,6 @@
 #ifndef PACK_U
 #define PACK_U 3
 #endif
-// equal-row peers by one ballot per row bit instead of __match_any_sync
-// (shorter latency chain; 4.566 -> 4.553 ms on c2)
-#ifndef PACK_BALLOT_MATCH
-#define PACK_BALLOT_MATCH 1
-#endif
-// phase C: a window of U elements that lies inside the current row skips the
-// per-element row-change test (no branch / reconvergence per element)
-#ifndef PACK_FASTWIN
-#define PACK_FASTWIN 1
-#endif
-// phase D: one warp per tail entry folds the head entries that continue its
-// row (no scans over empty entries, no zeroing of the boundary tiles)
-// phase C reads the sorted tile two records at a time (LDS.128); pieces are
-// padded by 16 B so they start 16-B aligned and the 4 groups of a warp hit
-// different banks.  Needs an even PACK_U.
-#ifndef PACK_PAIRS
-#define PACK_PAIRS 0
-#endif
-#define PACK_PAD (PACK_PAIRS ? 2 : 1)
-// phase A without per-item bounds tests on full tiles
-#ifndef PACK_FULL_TILE
-#define PACK_FULL_TILE 1
-#endif
-// cheaper ballot rounds (no per-bit guard, no select)
-#ifndef PACK_BALLOT2
-#define PACK_BALLOT2 1
-#endif
-#ifndef PACK_SIMPLE_D
-#define PACK_SIMPLE_D 1
-#endif
 
 namespace fc {
 
@@ -58,7 +28,7 @@ template <int LPG>
 struct PackPlan {
   static constexpr int G = kFBlock / LPG;
   static constexpr int P = kFTile / G;
-  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + PACK_PAD * G);
+  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + G);
   static constexpr size_t misc_bytes = 4 * (kFWarps + 4 + G);
   static constexpr size_t fixed_bytes = sorted_bytes + misc_bytes;
   __host__ __device__ static size_t hist_bytes(int64_t m) {
@@ -84,9 +54,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 
   extern __shared__ __align__(16) unsigned char smem[];
   const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
-#if PACK_BALLOT_MATCH
   const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
-#endif
   uint2 *s_sorted = reinterpret_cast<uint2 *>(smem);
   int *s_misc = reinterpret_cast<int *>(smem + PP::sorted_bytes);
   int *s_piece_bin = s_misc + kFWarps + 4;  // first bin of every piece
@@ -132,7 +100,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   const int lg = tid % LPG;
   const int col = lg * 4;
   const bool col_ok = RT > 0 ? true : col < R;
-  auto phys = [](int pos) { return pos + PACK_PAD * (pos / P); };
+  auto phys = [](int pos) { return pos + pos / P; };
   auto key_of = [&](const int4 &r) {
     const int lr = comp<MODE>(r) - irow0;
     return (lr >= 0 && lr < rows) ? lr : -1;
@@ -145,7 +113,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     // ---------------------------------------------------------------- A
     int4 rec[kFIPT];
     uint32_t slot[kFIPT];
-#if PACK_FULL_TILE
     if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -154,7 +121,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         if (a.do_remap) slot[j] = ld_stream_u32(a.slots + i);
       }
     } else
-#endif
     {
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -172,7 +138,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int e = j * kFBlock + tid;
-      if (PACK_FULL_TILE ? (cnt == kFTile || e < cnt) : e < cnt) {
+      if (cnt == kFTile || e < cnt) {
         if (a.do_remap) {
           remap_store<1, true, PEER>(a, slot[j], rec[j], rec[j], 0.f);
         }
@@ -195,10 +161,8 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
-#if PACK_BALLOT_MATCH
       // equal-row peers from one ballot per key bit (rows < 2^hbits)
       unsigned peers = __ballot_sync(0xffffffffu, k >= 0);
-#if PACK_BALLOT2
       // bits >= hbits are 0 for every valid lane, so extra rounds only drop
       // invalid lanes again: 5 fixed rounds for <= 32 rows, 6 for <= 64, else 8
       auto round = [&](int b) {
@@ -216,20 +180,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #pragma unroll
         for (int b = 0; b < 8; ++b) round(b);
       }
-#else
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {  // rows <= 256; the guard is warp-uniform
-        if (b < hbits) {
-          const bool bit = (k >> b) & 1;
-          const unsigned m = __ballot_sync(0xffffffffu, bit);
-          peers &= bit ? m : ~m;
-        }
-      }
-#endif
       const unsigned grp = k >= 0 ? peers : (1u << lane);
-#else
-      const unsigned grp = __match_any_sync(0xffffffffu, k >= 0 ? k : -1 - lane);
-#endif
       const int leader = __ffs(grp) - 1;
       int old = 0;
       if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
@@ -298,13 +249,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       s_bnd_row[2 * gi] = -1;
       s_bnd_row[2 * gi + 1] = -1;
     }
-#if !PACK_SIMPLE_D
-    if (col_ok) {
-      const float z[4] = {0.f, 0.f, 0.f, 0.f};
-      VecT<4>::store(s_bnd + (2 * gi) * R + col, z);
-      VecT<4>::store(s_bnd + (2 * gi + 1) * R + col, z);
-    }
-#endif
     const int pb = gi * P;
     const int pe = min(pb + P, nvalid);
     if (pb < pe) {
@@ -354,28 +298,17 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         pr.lo = f2_mul(f1.lo, f2.lo);
         pr.hi = f2_mul(f1.hi, f2.hi);
       };
-      const uint2 *sp = s_sorted + PACK_PAD * gi;  // pads of the pieces before gi
+      const uint2 *sp = s_sorted + gi;  // pad of piece gi
       int p = pb;
       for (; p + U <= pe; p += U) {
         uint2 q[U];
-#if PACK_PAIRS
-        static_assert(U % 2 == 0, "PACK_PAIRS needs an even PACK_U");
-#pragma unroll
-        for (int u = 0; u < U; u += 2) {
-          const uint4 q2 = *reinterpret_cast<const uint4 *>(sp + p + u);
-          q[u] = make_uint2(q2.x, q2.y);
-          q[u + 1] = make_uint2(q2.z, q2.w);
-        }
-#else
 #pragma unroll
         for (int u = 0; u < U; ++u) q[u] = sp[p + u];
-#endif
         f32x4p pr[U];
         if (col_ok) {
 #pragma unroll
           for (int u = 0; u < U; ++u) prod(q[u].x, pr[u]);
         }
-#if PACK_FASTWIN
         if (p + U <= nxt) {  // no row starts inside [p, p + U)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -386,7 +319,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
           }
           continue;
         }
-#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(p + u, __uint_as_float(q[u].y), pr[u]);
       }
@@ -407,7 +339,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     __syncthreads();
     PACK_PROBE(3);
     // ---------------------------------------------------------------- D
-#if PACK_SIMPLE_D
     // A row that crosses pieces a..b left a tail entry in piece a and a head
     // entry in each of a+1..b; its sum is tail(a) + head(a+1) + ... + head(b)
     // in piece order (the order of the scan-based fold it replaces).
@@ -428,55 +359,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         }
       }
     }
-#else
-    {
-      constexpr int E = (2 * G + kFWarps - 1) / kFWarps;
-      constexpr int RC = (LPG * 4 + 31) / 32;
-      const int ent0 = warp * E;
-      const int ent_end = min(2 * G, ent0 + E);
-      int prev = -1;
-      for (int e2 = ent0 - 1; e2 >= 0; --e2) {
-        const int r2 = s_bnd_row[e2];
-        if (r2 >= 0) {
-          prev = r2;
-          break;
-        }
-      }
-      for (int ent = ent0; ent < ent_end; ++ent) {
-        const int row = s_bnd_row[ent];
-        if (row < 0 || row == prev) {
-          if (row >= 0) prev = row;
-          continue;
-        }
-        prev = row;
-        int e3 = ent + 1;
-        while (e3 < 2 * G) {
-          const int r3 = s_bnd_row[e3];
-          if (r3 >= 0 && r3 != row) break;
-          ++e3;
-        }
-#pragma unroll
-        for (int q = 0; q < RC; ++q) {
-          const int c = q * 32 + lane;
-          if (c < R) {
-            float run = 0.f;
-            int e = ent;
-            for (; e + 4 <= e3; e += 4) {
-              const float x0 = s_bnd[e * R + c], x1 = s_bnd[(e + 1) * R + c];
-              const float x2 = s_bnd[(e + 2) * R + c], x3 = s_bnd[(e + 3) * R + c];
-              run += x0;
-              run += x1;
-              run += x2;
-              run += x3;
-            }
-            for (; e < e3; ++e) run += s_bnd[e * R + c];
-            if (direct) out_rows[row * R + c] = run;
-            else s_acc[row * R + c] += run;
-          }
-        }
-      }
-    }
-#endif
   }
   PACK_PROBE(4);
   if (!direct) {
