@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (bad) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
     }
     __syncwarp();
+    PACK_PROBE(0);
     // ---------------------------------------------------------------- B
     int *wh = s_hist + warp * hstride;
     // stable per-warp counting: the leader of each equal-row group reserves
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
-    PACK_PROBE(0);
+    PACK_PROBE(1);
     {
       int tot = 0;
       if (tid < rows) {
@@ -205,12 +206,17 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
+      // rows <= 32: warp 0 holds every row, so no cross-warp prefix (and no
+      // middle barrier) is needed
+      const bool one_warp = rows <= 32;
       if (lane == 31) s_misc[warp] = incl;
-      __syncthreads();
+      if (!one_warp) __syncthreads();
       int wpre = 0;
+      if (!one_warp) {
 #pragma unroll 4
-      for (int w = 0; w < kFWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
-      if (tid == kFBlock - 1) s_misc[kFWarps] = wpre + incl;
+        for (int w = 0; w < kFWarps; ++w) wpre += w < warp ? s_misc[w] : 0;
+      }
+      if (tid == (one_warp ? 31 : kFBlock - 1)) s_misc[kFWarps] = wpre + incl;
       if (tid < rows) {
         const int bstart = wpre + incl - tot;
         int base = bstart;
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(1);
+    PACK_PROBE(2);
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int x = comp<MODE>(rec[j]);
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(2);
+    PACK_PROBE(3);
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
     if (tid == 0 && t0 + kFTile < end) {
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(3);
+    PACK_PROBE(4);
     // ---------------------------------------------------------------- D
     // A row that crosses pieces a..b left a tail entry in piece a and a head
     // entry in each of a+1..b; its sum is tail(a) + head(a+1) + ... + head(b)
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
   }
-  PACK_PROBE(4);
+  
   if (!direct) {
     __syncthreads();
     float *dstp = part < 0 ? out_rows : partial_ws(a, chunk) + (int64_t)part * a.m * R;

@@ -71,4 +71,4 @@ if hasattr(L, "fc_debug_phase_cycles"):
     L.fc_debug_phase_cycles(buf, 1)
     tot = sum(buf)
     print("phase cycles (thread 0 of each CTA, mode 0 x5): " + ", ".join(
-        f"{n} {100 * v / tot:.1f}%" for n, v in zip(("A+B1", "B2", "B3", "C", "D"), buf)))
+        f"{n} {100 * v / tot:.1f}%" for n, v in zip(("D(prev)+A", "B1 rank", "B2 scan", "B3 scatter", "C"), buf)))
