@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   extern __shared__ __align__(16) unsigned char smem[];
   const int hstride = (int)((a.hist_rows + 3) / 4 * 4);
   const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
+  const bool hist_rows32 = a.hist_rows <= 32;
   uint2 *s_sorted = reinterpret_cast<uint2 *>(smem);
   int *s_misc = reinterpret_cast<int *>(smem + PP::sorted_bytes);
   int *s_piece_bin = s_misc + kFWarps + 4;  // first bin of every piece
@@ -154,6 +155,35 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     PACK_PROBE(0);
     // ---------------------------------------------------------------- B
     int *wh = s_hist + warp * hstride;
+#ifndef PACK_LANE_ROWS
+#define PACK_LANE_ROWS 1
+#endif
+    if (PACK_LANE_ROWS && hist_rows32) {
+      // <= 32 rows: lane r owns row r's count in this warp.  From the key-bit
+      // ballots lane r forms `own` = the lanes holding row r; an element's
+      // equal-row peers and its group's base are then one shuffle each from
+      // the lane owning its row -- no shared atomics, no leader election.
+      // Ranks are (count in earlier items) + (lower lanes in this item):
+      // the same stable order as the atomic path.
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        const int k = key_of(rec[j]);
+        unsigned own = __ballot_sync(0xffffffffu, k >= 0);
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+          const unsigned m = __ballot_sync(0xffffffffu, ((unsigned)k >> b) & 1u);
+          own &= m ^ ((((unsigned)lane >> b) & 1u) - 1u);
+        }
+        const int before = cnt;
+        cnt += __popc(own);
+        const int src = k & 31;
+        const unsigned peers = __shfl_sync(0xffffffffu, own, src);
+        const int base = __shfl_sync(0xffffffffu, before, src);
+        set_comp<MODE>(rec[j], k >= 0 ? (((base + __popc(peers & lt_mask)) << 8) | k) : -1);
+      }
+      if (lane < rows) wh[lane] = cnt;
+    } else {
     // stable per-warp counting: the leader of each equal-row group reserves
     // the group's run with one shared atomic (returns the old count) and
     // broadcasts it; a warp's shared atomics to one address execute in issue
@@ -187,6 +217,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
       old = __shfl_sync(0xffffffffu, old, leader);
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
+    }
     }
     __syncthreads();
     PACK_PROBE(1);
