@@ -265,6 +265,28 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     // as (rank << 8 | local row) until B3 restores the coordinate -- keeps
     // the 8 ranks out of registers.
     int *wh = s_hist + warp * hstride;
+    if (a.hist_rows <= 32) {
+      // row-owner lanes (pack_kernel.cuh): lane r counts row r; peers and
+      // group base come from the owner lane by shuffle
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        const int k = key_of(rec[j]);
+        unsigned own = __ballot_sync(0xffffffffu, k >= 0);
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+          const unsigned m = __ballot_sync(0xffffffffu, ((unsigned)k >> b) & 1u);
+          own &= m ^ ((((unsigned)lane >> b) & 1u) - 1u);
+        }
+        const int before = cnt;
+        cnt += __popc(own);
+        const int src = k & 31;
+        const unsigned peers = __shfl_sync(0xffffffffu, own, src);
+        const int base = __shfl_sync(0xffffffffu, before, src);
+        set_comp<MODE>(rec[j], k >= 0 ? (((base + __popc(peers & lt_mask)) << 8) | k) : -1);
+      }
+      if (lane < rows) wh[lane] = cnt;
+    } else
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
