@@ -47,7 +47,7 @@ struct FastPlan {
   static constexpr size_t sorted_bytes = sizeof(int4) * (kFTile + G);
   static constexpr size_t sval_bytes = EMB ? 0 : sizeof(float) * (kFTile + G);
   static constexpr size_t misc_bytes = 4 * (kFWarps + 4);
-  static constexpr size_t fixed_bytes = sorted_bytes + sval_bytes + misc_bytes;
+  static constexpr size_t fixed_bytes = (sorted_bytes + sval_bytes + misc_bytes + 15) / 16 * 16;
   // dynamic tail: per-warp row histograms (m ints each), boundary entries,
   // the m x R accumulator tile
   __host__ __device__ static size_t hist_bytes(int64_t m) { return sizeof(int) * kFWarps * ((m + 3) / 4 * 4); }

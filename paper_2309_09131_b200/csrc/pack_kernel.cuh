@@ -30,7 +30,7 @@ struct PackPlan {
   static constexpr int P = kFTile / G;
   static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + G);
   static constexpr size_t misc_bytes = 4 * (kFWarps + 4 + G);
-  static constexpr size_t fixed_bytes = sorted_bytes + misc_bytes;
+  static constexpr size_t fixed_bytes = (sorted_bytes + misc_bytes + 15) / 16 * 16;
   __host__ __device__ static size_t hist_bytes(int64_t m) {
     return sizeof(int) * kFWarps * ((m + 3) / 4 * 4);
   }
