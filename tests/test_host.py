@@ -183,3 +183,21 @@ def test_frostt_parse_and_write_match_reference():
         with pytest.raises(fio.FrosttParseError) as e:
             fio.parse_frostt(bad)
         assert e.value.lineno == line
+
+
+def test_lean_build_rejects_unsupported_layouts():
+    """build_device_sharded_lean validates before touching the device: 16-B
+    records of a 2/3-mode tensor, the declared nonzero count, <= 32-bit Morton keys."""
+    import pytest
+    import torch
+    from paper_2309_09131_b200 import device_params
+    from paper_2309_09131_b200.layout import build_device_sharded_lean
+    rec = torch.zeros((10, 4), dtype=torch.int32)
+    with pytest.raises(ValueError, match="16-B records"):
+        build_device_sharded_lean(torch.zeros((10, 8), dtype=torch.int32),
+                                  device_params((5, 5, 5, 5), 10, 8), device="cpu")
+    with pytest.raises(ValueError, match="different nonzero count"):
+        build_device_sharded_lean(rec, device_params((50, 50, 50), 11, 8), device="cpu")
+    with pytest.raises(ValueError, match="Morton key"):
+        build_device_sharded_lean(rec, device_params((1 << 20, 1 << 20, 1 << 20), 10, 8, m=[1, 1, 1]),
+                                  device="cpu")
