@@ -35,12 +35,24 @@ inline bool pack_enabled() {
   return v == 1;
 }
 
+inline bool pack_wide_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("FLYCOO_PACK_WIDE");
+    v = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NM, int MODE, int LPG, int RT, bool PEER>
 int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   if constexpr (NM == 3) {
     // 8-byte sorted records when the two input coordinates fit 32 bits
     if (a.pack_shift > 0 && (PEER || kernel_kind() == 1) && pack_enabled())
       return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
+    // wider coordinates: {c_w1, c_w2} + value array, rows from the bins
+    if (a.pack_shift == 0 && (PEER || kernel_kind() == 1) && pack_wide_enabled())
+      return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
   // multi-GPU fused exchange: tile kernel only; direct chunks (hist_rows >
   // tile_rows) exist only in the tile kernel

@@ -24,11 +24,16 @@
 
 namespace fc {
 
-template <int LPG>
+// WIDE: 3-mode tensors whose input coordinates do NOT fit 32 bits together
+// (c4: 21 + 21 bits): the sorted tile holds {c_w1, c_w2} words plus a
+// separate value array (12 B per element instead of the tile kernel's 16,
+// rows from the bins as here)
+template <int LPG, bool WIDE = false>
 struct PackPlan {
   static constexpr int G = kFBlock / LPG;
   static constexpr int P = kFTile / G;
-  static constexpr size_t sorted_bytes = sizeof(uint2) * (kFTile + G);
+  static constexpr size_t sval_offset = sizeof(uint2) * (kFTile + G);
+  static constexpr size_t sorted_bytes = sval_offset + (WIDE ? sizeof(float) * (kFTile + G) : 0);
   static constexpr size_t misc_bytes = 4 * (kFWarps + 4 + G);
   static constexpr size_t fixed_bytes = (sorted_bytes + misc_bytes + 15) / 16 * 16;
   __host__ __device__ static size_t hist_bytes(int64_t m) {
@@ -40,9 +45,9 @@ struct PackPlan {
   }
 };
 
-template <int MODE, int LPG, int RT, bool PEER = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const __grid_constant__ ModeArgs a) {
-  using PP = PackPlan<LPG>;
+  using PP = PackPlan<LPG, WIDE>;
   constexpr int G = PP::G;
   constexpr int P = PP::P;
   constexpr int U = PACK_U;
@@ -57,6 +62,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   const int hbits = 32 - __clz((int)(a.hist_rows > 1 ? a.hist_rows - 1 : 1));
   const bool hist_rows32 = a.hist_rows <= 32;
   uint2 *s_sorted = reinterpret_cast<uint2 *>(smem);
+  float *s_sval = reinterpret_cast<float *>(smem + PP::sval_offset);  // WIDE only
   int *s_misc = reinterpret_cast<int *>(smem + PP::sorted_bytes);
   int *s_piece_bin = s_misc + kFWarps + 4;  // first bin of every piece
   unsigned char *tail = smem + PP::fixed_bytes;
@@ -269,8 +275,13 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (x >= 0) {
         const int k = x & 255;
         const int pos = wh[k] + (x >> 8);
-        const uint32_t pk = ((uint32_t)comp<W1>(rec[j]) << shift) | (uint32_t)comp<W2>(rec[j]);
-        s_sorted[phys(pos)] = make_uint2(pk, (uint32_t)rec[j].w);
+        if constexpr (WIDE) {
+          s_sorted[phys(pos)] = make_uint2((uint32_t)comp<W1>(rec[j]), (uint32_t)comp<W2>(rec[j]));
+          s_sval[phys(pos)] = __int_as_float(rec[j].w);
+        } else {
+          const uint32_t pk = ((uint32_t)comp<W1>(rec[j]) << shift) | (uint32_t)comp<W2>(rec[j]);
+          s_sorted[phys(pos)] = make_uint2(pk, (uint32_t)rec[j].w);
+        }
       }
     }
     __syncthreads();
@@ -328,28 +339,35 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       const float *f1b = a.fac[W1] + col;
       const float *f2b = a.fac[W2] + col;
       const uint32_t rstride = (uint32_t)(RT > 0 ? RT : R);
-      auto prod = [&](uint32_t pk, f32x4p &pr) {
-        const uint32_t c1 = pk >> shift, c2 = pk & lowmask;
+      // q = {packed coordinates, value bits} or, WIDE, {c_w1, c_w2} (+ s_sval)
+      auto prod = [&](const uint2 &q, f32x4p &pr) {
+        const uint32_t c1 = WIDE ? q.x : q.x >> shift, c2 = WIDE ? q.y : q.x & lowmask;
         const f32x4p f1 = f4p(__ldg(reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride)));
         const f32x4p f2 = f4p(__ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride)));
         pr.lo = f2_mul(f1.lo, f2.lo);
         pr.hi = f2_mul(f1.hi, f2.hi);
       };
       const uint2 *sp = s_sorted + gi;  // pad of piece gi
+      const float *svp = s_sval + gi;
+      auto val = [&](const uint2 &q, int at) { return WIDE ? svp[at] : __uint_as_float(q.y); };
       int p = pb;
       for (; p + U <= pe; p += U) {
         uint2 q[U];
+        float vq[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) q[u] = sp[p + u];
+        for (int u = 0; u < U; ++u) {
+          q[u] = sp[p + u];
+          vq[u] = val(q[u], p + u);
+        }
         f32x4p pr[U];
         if (col_ok) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) prod(q[u].x, pr[u]);
+          for (int u = 0; u < U; ++u) prod(q[u], pr[u]);
         }
         if (p + U <= nxt) {  // no row starts inside [p, p + U)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const float v = __uint_as_float(q[u].y);
+            const float v = vq[u];
             const f32x2 vv = f2_pack(v, v);
             acc.lo = f2_fma(vv, pr[u].lo, acc.lo);
             acc.hi = f2_fma(vv, pr[u].hi, acc.hi);
@@ -357,13 +375,13 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
           continue;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) consume(p + u, __uint_as_float(q[u].y), pr[u]);
+        for (int u = 0; u < U; ++u) consume(p + u, vq[u], pr[u]);
       }
       for (; p < pe; ++p) {
         const uint2 q = sp[p];
         f32x4p pr;
-        if (col_ok) prod(q.x, pr);
-        consume(p, __uint_as_float(q.y), pr);
+        if (col_ok) prod(q, pr);
+        consume(p, val(q, p), pr);
       }
       const bool tail = pe < nvalid && nxt > pe;
       if (tail && !head) {
@@ -413,10 +431,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 #endif
 }
 
-template <int MODE, int LPG, int RT, bool PEER = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
-  const size_t smem = PackPlan<LPG>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER>;
+  const size_t smem = PackPlan<LPG, WIDE>::total(a.rank, a.tile_rows, a.hist_rows);
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
