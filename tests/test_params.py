@@ -39,10 +39,10 @@ def test_device_params_cover_dims():
     assert all(m * k >= d for m, k, d in zip(p.m, p.k, p.dims))
     q = device_params((46, 239172, 239172), 10, 16, acc_tile_bytes=8192)
     assert q.m[0] == 46 and q.k[0] == 1
-    # per-mode choice: 4 KB tiles for large (c2) or very sparse (c3 modes 1-2) super-shards,
-    # 8 KB otherwise (c4); always covering the dims
+    # 3-mode tensors: 4 KB tiles (c2, c4); 4-mode: per mode, 4 KB tiles for large or very
+    # sparse (c3 modes 1-3) super-shards, 8 KB otherwise (c3 mode 0); always covering the dims
     assert device_params((12092, 9184, 28818), 76_900_000, 32).m == (32, 32, 32)
-    assert device_params((4821207, 1774269, 1805187), 1_740_000_000, 32).m == (64, 64, 64)
+    assert device_params((4821207, 1774269, 1805187), 1_740_000_000, 32).m == (32, 32, 32)
     c3 = device_params((532924, 17262471, 2480308, 1443), 140_000_000, 32)
     assert c3.m == (64, 32, 32, 32)
     assert all(m * k >= d for m, k, d in zip(c3.m, c3.k, c3.dims))
