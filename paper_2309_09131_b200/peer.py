@@ -73,7 +73,7 @@ class PeerModePlan:
 # its tile passes' fixed work (barriers, histogram scan, boundary fold) and its
 # accumulator tile however few nonzeros it holds, so a GPU whose range is the
 # Zipf tail (many small super-shards) is slower than its nonzero share says.
-CHUNK_WEIGHT = int(os.environ.get("FLYCOO_CHUNK_WEIGHT", "4096"))
+CHUNK_WEIGHT = int(os.environ.get("FLYCOO_CHUNK_WEIGHT", "2048"))
 
 
 def partition_chunks(chunk_start: np.ndarray, world: int, chunk_weight: int | None = None) -> np.ndarray:

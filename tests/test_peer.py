@@ -131,7 +131,7 @@ def test_chunk_partition_balances_a_heavy_super_shard():
         # default: nonzeros + a fixed cost per chunk, balanced within one chunk's cost
         cb = partition_chunks(cs, world)
         nch = len(cs) - 1
-        kw = 4096
+        kw = 2048
         costs = np.diff(cs[cb]) + kw * np.diff(cb)
         assert costs.max() <= (len(subs) + kw * nch) / world + 2048 + kw, (world, costs)
         gpu = np.repeat(np.arange(world), np.diff(cb))
