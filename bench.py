@@ -245,7 +245,10 @@ def run_ours(args, rank, world, local):
     # FLYCOO_ACC_TILE_BYTES: one accumulator-tile size for every mode (experiments);
     # default: chosen per mode (params._auto_rows)
     tile_env = os.environ.get("FLYCOO_ACC_TILE_BYTES")
-    params = device_params(dims, nnz, R, acc_tile_bytes=int(tile_env) if tile_env else None)
+    # FLYCOO_SHARD_G: shard size g (experiments; default device_params' 32768)
+    g_env = os.environ.get("FLYCOO_SHARD_G")
+    params = device_params(dims, nnz, R, acc_tile_bytes=int(tile_env) if tile_env else None,
+                           **({"g": int(g_env)} if g_env else {}))
     t0 = time.perf_counter()
     if lean:
         from paper_2309_09131_b200.layout import build_device_sharded_lean
