@@ -450,3 +450,29 @@ def test_config5_law_every_row():
                    what=f"c5 law mode {n}")
     end = host_records(st)
     assert np.array_equal(start[0], end[0]) and np.array_equal(start[1], end[1])
+
+
+@pytest.mark.parametrize("cfg,nnz", [(3, 2_000_000), (4, 3_000_000)])
+def test_config_law_every_row(cfg, nnz):
+    """Configs 3 (4 modes, 17M-row sparse mode: direct chunks) and 4 (every
+    mode on the WIDE packed kernel: 21-23-bit coordinates) with their dims and
+    laws at a few million nonzeros: every output row of every mode against the
+    oracle, and the cycle identity."""
+    from paper_2309_09131_b200.synth import CONFIGS
+    c = CONFIGS[cfg]
+    dims = tuple(c["dims"])
+    coords, vals = zipf_tensor(dims, nnz, seed=cfg, exponents=c["law"])
+    subs = coords.cpu().numpy().astype(np.int64)
+    v64 = vals.cpu().numpy().astype(np.float64)
+    params = device_params(dims, nnz, 32)
+    st = build_device_sharded(coords, vals, params)
+    smap = schedule_super_shards(st.plan, 1)
+    fs = factors_f32(dims, 32, 1000 + cfg)
+    dfs = DeviceFactorSet.from_host(fs)
+    start = host_records(st)
+    for n in range(len(dims)):
+        out = mttkrp_mode(st, dfs, n, smap)
+        assert_rel(out.double().cpu().numpy(), oracle.reference_mttkrp(subs, v64, fs, n),
+                   what=f"c{cfg} law mode {n}")
+    end = host_records(st)
+    assert np.array_equal(start[0], end[0]) and np.array_equal(start[1], end[1])
