@@ -271,6 +271,7 @@ def run_ours(args, rank, world, local):
     updated = cfg["semantics"] == "updated"
     exchange = os.environ.get("FLYCOO_EXCHANGE", "p2p")
     dt = None
+    fallback = None  # why the fused peer exchange was not used (N > 1)
     if world > 1:
         # partitioned sweep: every rank builds the same global layout, keeps
         # its slices + static exchange plan, and frees the rest
@@ -283,9 +284,24 @@ def run_ours(args, rank, world, local):
                                                 peer_sweep_all_modes)
         t0 = time.perf_counter()
         if exchange == "p2p":
-            dt = PeerShardedTensor(st, world, rank)
-            dt.connect()
-        else:
+            # the fused exchange maps every peer's buffers (CUDA IPC over
+            # NVLink); if any rank cannot, every rank falls back to NCCL
+            try:
+                dt = PeerShardedTensor(st, world, rank)
+                dt.connect()
+                ok = 1
+            except Exception as e:  # noqa: BLE001 -- reported, then the NCCL path
+                dt, ok, fallback = None, 0, f"{type(e).__name__}: {e}"[:200]
+            flag = torch.tensor([ok], device="cpu" if backend == "gloo" else dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                if dt is not None:
+                    dt.close()
+                fallback = fallback or "a peer could not map the IPC buffers"
+                print(f"[bench] fused peer exchange unavailable ({fallback}); using NCCL",
+                      file=sys.stderr)
+                exchange = "nccl"
+        if exchange != "p2p":
             dt = DistShardedTensor(st, world, rank)
         plan_s = time.perf_counter() - t0
         del st
@@ -485,7 +501,8 @@ def run_ours(args, rank, world, local):
                         "memory, CUDA IPC) + peer pull of updated factor rows"
                         if exchange == "p2p" else
                         f"dp{world}: per-mode super-shard row ranges, NCCL all_to_all_single remap + "
-                        "all_gather_into_tensor of updated factor rows"),
+                        "all_gather_into_tensor of updated factor rows"
+                        + (f" (fused peer exchange unavailable: {fallback})" if fallback else "")),
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
                        "build": "lean (bucketed generator, layout.build_device_sharded_lean)" if lean else "regular",
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
