@@ -152,10 +152,14 @@ def reduce_plan(nch: np.ndarray, part_base: np.ndarray, fan: int = REDUCE_FAN):
     return r1, r2, slot
 
 
-def default_chunk_elems(nnz: int, tile: int = 2048) -> int:
+def default_chunk_elems(nnz: int, tile: int = 2048, avg_ss: float = 0.0) -> int:
     """Chunk size: 8192 elements, smaller for small tensors so that every
-    SM gets work (multiples of the 2048-element tile)."""
-    cap = int(os.environ.get("FLYCOO_CHUNK", "8192"))
+    SM gets work (multiples of the 2048-element tile); 32768 for modes whose
+    super-shards average >= 400k nonzeros (c5: a quarter of the partial tiles
+    to write and reduce, 45.8 -> 44.9 ms at 1B nonzeros; c2 and c4 are
+    neutral or slower with larger chunks and stay below the threshold)."""
+    env = os.environ.get("FLYCOO_CHUNK")
+    cap = int(env) if env else (32768 if avg_ss >= 400_000 else 8192)
     want = _cdiv(max(int(nnz), 1), 148 * 4)
     return int(min(cap, max(tile, _cdiv(want, tile) * tile)))
 
@@ -248,7 +252,9 @@ def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elem
                         int(r2.shape[0]), nparts, ws, ws2, C)
     if smem:
         if chunk_elems is None:
-            chunk_elems = default_chunk_elems(nnz, tile)
+            # (3-mode tensors only: c3's 4-mode tile kernel was slower with 32k chunks)
+            chunk_elems = default_chunk_elems(
+                nnz, tile, avg_ss=nnz / max(k, 1) if params.num_modes == 3 else 0.0)
         C = int(chunk_elems)
         nch = -(-counts // C)
     else:
