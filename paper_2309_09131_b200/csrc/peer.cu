@@ -139,9 +139,19 @@ int fc_stream_wait(const void *flag, uint32_t value, void *stream) {
     set_error("cuStreamWaitValue32 unavailable");
     return FC_ERR_CUDA;
   }
-  CUresult r = fn(reinterpret_cast<CUstream>(stream),
-                  reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)), value,
-                  CU_STREAM_WAIT_VALUE_GEQ);
+  // FLUSH: the peers' NVLink stores that precede their flag write are visible
+  // to this stream's later kernels (devices without remote-write flushing
+  // reject the flag: plain GEQ wait, remembered)
+  static int flush_ok = 1;
+  CUresult r = CUDA_ERROR_INVALID_VALUE;
+  if (flush_ok) {
+    r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)),
+           value, CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH);
+    if (r == CUDA_ERROR_INVALID_VALUE || r == CUDA_ERROR_NOT_SUPPORTED) flush_ok = 0;
+  }
+  if (!flush_ok)
+    r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)),
+           value, CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) {
     set_error("cuStreamWaitValue32 failed (%d)", (int)r);
     return FC_ERR_CUDA;
