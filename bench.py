@@ -34,6 +34,7 @@ sys.path.insert(0, str(ROOT))
 # the billion-nonzero configs build near the HBM limit: avoid fragmentation
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
+CPU_FULL_MAX = 80_000_000  # whole-workload CPU baseline up to c2's 76.9M nonzeros
 METRIC = "all-mode spMTTKRP+remap sweep time & nnz/s at R=32; % HBM roofline; 1/2/4/8 GPU"
 UNIT = "nnz/s"
 
@@ -137,15 +138,61 @@ def describe(cfg_index: int, cfg: dict) -> str:
             f"{cfg['semantics']}-factor sweep, fp32 values/factors U(0,1)")
 
 
-def kernel_name(N: int, dims, rank: int) -> str:
-    """The K1 instance the library dispatches for this shape (dispatch.cuh)."""
-    if os.environ.get("FLYCOO_KERNEL") in ("warp", "pipe"):
-        return f"mode_pass_{os.environ['FLYCOO_KERNEL']}_kernel"
-    if N == 3 and rank % 4 == 0 and rank <= 64 and os.environ.get("FLYCOO_PACK") != "0":
-        w = [(d - 1).bit_length() for d in dims]
-        if all(sum(w) - w[n] <= 32 for n in range(3)):
-            return "mode_pass_pack_kernel (8-B sorted records)"
-    return "mode_pass_fast_kernel"
+def kernel_names(st, rank: int) -> list:
+    """The K1 instance the library dispatches for each mode (mode_pass.cu
+    dispatch + dispatch.cuh): the general kernel when the accumulator tile is
+    not in shared memory or the shape is off the fast path; for 3-mode
+    tensors the packed kernel (8-B sorted records when the two input
+    coordinates fit 32 bits, else the WIDE {c_w1, c_w2} + value variant);
+    otherwise the tile kernel."""
+    dims = st.params.dims
+    N = len(dims)
+    names = []
+    for n in range(N):
+        w = st.mode_work(n, rank)
+        fast = (w.acc_in_smem and w.hist_rows <= 256 and 2 <= N <= 4 and rank % 4 == 0
+                and rank <= 64)
+        if not fast:
+            names.append("mode_pass_kernel (general)")
+        elif N == 3 and os.environ.get("FLYCOO_PACK") != "0":
+            w1, w2 = (1, 2) if n == 0 else (0, 2) if n == 1 else (0, 1)
+            b1, b2 = ((dims[w1] - 1).bit_length(), (dims[w2] - 1).bit_length())
+            if b2 >= 1 and b1 + b2 <= 32:
+                names.append("mode_pass_pack_kernel (8-B sorted records)")
+            elif os.environ.get("FLYCOO_PACK_WIDE") != "0":
+                names.append("mode_pass_pack_kernel WIDE ({c_w1, c_w2} + value)")
+            else:
+                names.append("mode_pass_fast_kernel")
+        else:
+            names.append("mode_pass_fast_kernel")
+    return names
+
+
+def kernel_sources_hash() -> str:
+    """sha256 (16 hex) of the CUDA sources: stamps the ncu traffic record so
+    a number captured on other kernels is never reported."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted((ROOT / "paper_2309_09131_b200" / "csrc").glob("*.cu*")):
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(cfg_index: int, nnz: int, params) -> tuple:
+    """DRAM bytes per mode-pass launch from profiles/traffic.json, only when
+    it was captured on these kernel sources and this workload
+    (tools/traffic_from_ncu.py writes it); else (None, why)."""
+    tpath = ROOT / "profiles" / "traffic.json"
+    if not tpath.exists():
+        return None, "no profiles/traffic.json"
+    tj = json.loads(tpath.read_text())
+    want = {"config": cfg_index, "nnz": nnz, "params_m": list(params.m), "params_g": params.g,
+            "kernel_sources": kernel_sources_hash()}
+    bad = [k for k, v in want.items() if tj.get(k) != v]
+    if bad:
+        return None, f"profiles/traffic.json does not match this run ({', '.join(bad)})"
+    return tj.get("dram_bytes_per_launch"), tj.get("source")
 
 
 def compulsory_bytes(nnz: int, dims, rank: int):
@@ -157,30 +204,45 @@ def compulsory_bytes(nnz: int, dims, rank: int):
     return [b] * N
 
 
-def cpu_sample(cfg_index: int, cfg: dict, sample: int):
-    """First `sample` distinct nonzeros of the workload (a prefix of it:
-    the generator keeps the first distinct draws in draw order)."""
+def host_tensor(cfg_index: int, cfg: dict, nnz: int):
+    """The workload's first `nnz` distinct nonzeros on the host (int64 subs,
+    fp32-valued float64 vals): generated on the GPU when there is one (the
+    same generator as our arm, copied back), else by its numpy twin
+    (synth.zipf_tensor_host / synth_tensor: identical output, tested)."""
     import numpy as np
-    from paper_2309_09131_b200.synth import synth_tensor, zipf_tensor_host
+    import torch
+    from paper_2309_09131_b200.synth import config_tensor, synth_tensor, zipf_tensor_host
     if cfg["law"] is None:
-        subs, vals = synth_tensor(cfg["dims"], sample, seed=cfg_index, skew=0.0)
+        subs, vals = synth_tensor(cfg["dims"], nnz, seed=cfg_index, skew=0.0)
         return subs, vals.astype(np.float32).astype(np.float64)
-    subs, vals = zipf_tensor_host(cfg["dims"], sample, seed=cfg_index, exponents=cfg["law"])
+    if torch.cuda.is_available() and len(cfg["dims"]) <= 4:
+        coords, vals = config_tensor(cfg_index, device="cuda", nnz=nnz)
+        subs = coords.cpu().numpy().astype(np.int64)
+        v = vals.cpu().numpy().astype(np.float64)
+        del coords, vals
+        torch.cuda.empty_cache()
+        return subs, v
+    subs, vals = zipf_tensor_host(cfg["dims"], nnz, seed=cfg_index, exponents=cfg["law"])
     return subs, vals.astype(np.float64)
 
 
-def cpu_baseline(cfg_index: int, cfg: dict, sample: int, steps: int, warmup: int) -> dict:
+def cpu_baseline(cfg_index: int, cfg: dict, sample: int, steps: int, warmup: int,
+                 tensor=None) -> dict:
     """The reference algorithm's CPU port (oracle/: restated mode_worker with
-    one pthread per core, LPT schedule, reference params) timed per sweep."""
+    one pthread per core, LPT schedule, reference params select_params(nu =
+    cores, 32 MiB, R) as the reference's run_bench, bench.py:94-160) timed
+    per sweep (the reference times the sweep only, bench.py:129-147)."""
     import numpy as np
     import oracle
     from paper_2309_09131_b200.params import select_params
     threads = os.cpu_count() or 1
-    subs, vals = cpu_sample(cfg_index, cfg, sample)
+    subs, vals = tensor if tensor is not None else host_tensor(cfg_index, cfg, sample)
     R = cfg["rank"]
     params = select_params(cfg["dims"], len(vals), threads, 32 << 20, R)
+    t0 = time.perf_counter()
     L = oracle.canonical_build(subs, vals, cfg["dims"], params.m, params.k, params.g)
     t = oracle.OracleTensor(L, "reference", nu=threads)
+    build_s = time.perf_counter() - t0
     rng = np.random.Generator(np.random.Philox(1000 + cfg_index))
     f0 = [rng.random((d, R)).astype(np.float32).astype(np.float64) for d in cfg["dims"]]
     N = len(cfg["dims"])
@@ -200,11 +262,14 @@ def cpu_baseline(cfg_index: int, cfg: dict, sample: int, steps: int, warmup: int
         sweep()
         times.append(time.perf_counter() - t0)
     med = statistics.median(times)
+    whole = len(vals) == cfg["nnz"]
+    what = ("the whole workload" if whole else
+            f"first {len(vals):,} distinct nonzeros of the workload (prefix)")
     return {"value": N * len(vals) / med, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"first {len(vals):,} distinct nonzeros of the same workload (prefix), "
-                       f"reference params select_params(nu={threads}, 32 MiB, R={R}) -> "
-                       f"m={list(params.m)}, g={params.g}; median of {steps} sweeps"),
-            "ms_per_sweep": med * 1e3}
+            "sample": (f"{what}; reference params select_params(nu={threads}, 32 MiB, R={R}) -> "
+                       f"m={list(params.m)}, g={params.g}; {cfg['semantics']}-factor sweep, "
+                       f"median of {steps} sweeps after {warmup} warm-up"),
+            "ms_per_sweep": med * 1e3, "nnz": len(vals), "build_s": round(build_s, 2)}
 
 
 # ---------------------------------------------------------------- our arm
@@ -258,16 +323,28 @@ def run_ours(args, rank, world, local):
         coords, vals = config_tensor(args.config, device=dev, nnz=nnz)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
+    # the CPU baseline runs on the whole workload when it is small enough for
+    # the host port (c1, c2: <= 80M nonzeros, ~20 GB of host arrays), else on a
+    # bounded prefix of it
+    cpu_sample_n = None
+    host_copy = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_sample_n = args.cpu_sample or (nnz if nnz <= CPU_FULL_MAX else 8_000_000)
+        if cpu_sample_n == nnz and not lean:
+            host_copy = (coords.cpu().numpy().astype(np.int64), vals.cpu().numpy().astype(np.float64))
     t0 = time.perf_counter()
     if lean:
         st = build_device_sharded_lean(rec, params, device=dev)
         del rec
     else:
-        st = build_device_sharded(coords, vals, params, device=dev)
+        # generator output is duplicate-free by construction (first occurrences)
+        st = build_device_sharded(coords, vals, params, device=dev, check_duplicates=False)
         del coords, vals
     build_s = time.perf_counter() - t0
+    build_stages = dict(st.build_stages)
     smap = schedule_super_shards(st.plan, 1)
-    factors = DeviceFactorSet.random(dims, R, seed=1000 + args.config, device=dev)
+    kernels = kernel_names(st, R)
+    factors = DeviceFactorSet.random_device(dims, R, seed=1000 + args.config, device=dev)
     updated = cfg["semantics"] == "updated"
     exchange = os.environ.get("FLYCOO_EXCHANGE", "p2p")
     dt = None
@@ -285,18 +362,31 @@ def run_ours(args, rank, world, local):
         t0 = time.perf_counter()
         if exchange == "p2p":
             # the fused exchange maps every peer's buffers (CUDA IPC over
-            # NVLink); if any rank cannot, every rank falls back to NCCL
+            # NVLink); if any rank cannot, every rank falls back to NCCL.  Two
+            # agreements keep the collectives matched: construction (local
+            # allocations) first, then the collective connect.
+            def agree(ok: int) -> bool:
+                flag = torch.tensor([ok], device="cpu" if backend == "gloo" else dev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                return int(flag.item()) == 1
+
             try:
                 dt = PeerShardedTensor(st, world, rank)
-                dt.connect()
-                ok = 1
             except Exception as e:  # noqa: BLE001 -- reported, then the NCCL path
-                dt, ok, fallback = None, 0, f"{type(e).__name__}: {e}"[:200]
-            flag = torch.tensor([ok], device="cpu" if backend == "gloo" else dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag.item()) == 0:
+                dt, fallback = None, f"{type(e).__name__}: {e}"[:200]
+            connected = False
+            if agree(1 if dt is not None else 0):
+                try:
+                    dt.connect()
+                    connected = True
+                except Exception as e:  # noqa: BLE001
+                    fallback = f"{type(e).__name__}: {e}"[:200]
+                if not agree(1 if connected else 0):
+                    connected = False
+            if not connected:
                 if dt is not None:
                     dt.close()
+                    dt = None
                 fallback = fallback or "a peer could not map the IPC buffers"
                 print(f"[bench] fused peer exchange unavailable ({fallback}); using NCCL",
                       file=sys.stderr)
@@ -417,12 +507,7 @@ def run_ours(args, rank, world, local):
     # + the unpack (NCCL exchange) or the row gather (fused exchange) per mode
     launches_per_step = sum(src.mode_work(n, R).launches + (1 if dt is not None else 0)
                             for n in range(N))
-    traffic = None
-    tpath = ROOT / "profiles" / "traffic.json"
-    if tpath.exists():
-        tj = json.loads(tpath.read_text())
-        if tj.get("config") == args.config and tj.get("nnz") == nnz:
-            traffic = tj.get("dram_bytes_per_launch")
+    traffic, traffic_src = measured_traffic(args.config, nnz, params)
 
     # end to end through the public API: pinned host factors in, results out
     e2e = None
@@ -477,9 +562,11 @@ def run_ours(args, rank, world, local):
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms, "path": path}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or min(nnz, 8_000_000)
-        cpu = cpu_baseline(args.config, cfg, sample, steps=3, warmup=1)
+    if cpu_sample_n is not None:
+        del graph, peer_graph, st, factors
+        torch.cuda.empty_cache()
+        cpu = cpu_baseline(args.config, cfg, cpu_sample_n, steps=3, warmup=1, tensor=host_copy)
+        del host_copy
 
     if rank == 0:
         line = {
@@ -504,14 +591,18 @@ def run_ours(args, rank, world, local):
                         "all_gather_into_tensor of updated factor rows"
                         + (f" (fused peer exchange unavailable: {fallback})" if fallback else "")),
                        "gen_s": round(gen_s, 3), "build_s": round(build_s, 3),
+                       # build stages (CUDA events; PAPER.md:762 reports super-shard
+                       # generation, Morton ordering and shard generation)
+                       "build_stages_s": {k: round(v, 4) for k, v in build_stages.items()},
                        "build": "lean (bucketed generator, layout.build_device_sharded_lean)" if lean else "regular",
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
                        # median over the measured sweeps of each mode pass
                        "mode_ms": [round(1e3 * statistics.median(mode_secs[n::N]), 4)
                                    for n in range(N)] if mode_secs else []},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": kernel_name(N, dims, R) + " (+ reduce_level_kernel)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "; ".join(f"mode {n}: {k}" for n, k in enumerate(kernels))
+                                   + " (+ reduce_level_kernel)",
                          "algorithmic_bytes_per_launch": per_mode[0], "peak_source": peak_src,
                          "timing_basis": basis},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
@@ -525,24 +616,27 @@ def run_ours(args, rank, world, local):
 # ---------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world, local):
-    """The reference's CPU implementation of the path (oracle/ port, all host
-    threads) on a bounded prefix of this arm's workload; rank 0 only."""
+    """The reference's CPU implementation of the path (oracle/ port of the
+    numba mode_worker, all host threads, the reference's own parameter
+    choice) on this arm's workload -- the whole tensor for c1/c2, a bounded
+    prefix for the billion-nonzero configs; rank 0 only."""
     if rank != 0:
         return
     cfg = workload(args.config, args.nnz)
-    # bounded sample: 8M nonzeros (~0.5 s per sweep on a 16-core host) up to
-    # ~150 sweeps, shrinking beyond that so the reference arm stays ~1-2 min
-    budget = int(8_000_000 * 150 / max(args.steps + args.warmup, 150))
-    sample = args.cpu_sample or min(cfg["nnz"], max(200_000, budget))
-    res = cpu_baseline(args.config, cfg, sample, steps=max(args.steps, 1), warmup=max(args.warmup, 0))
+    nnz = cfg["nnz"]
+    sample = args.cpu_sample or (nnz if nnz <= CPU_FULL_MAX else 8_000_000)
+    res = cpu_baseline(args.config, cfg, sample, steps=max(args.steps, 1),
+                       warmup=max(args.warmup, 0))
     N = len(cfg["dims"])
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_sweep"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
+        # the same config keys as our arm's line (same workload, whole tensor)
         "config": {"workload": describe(args.config, cfg), "config_index": args.config,
-                   "sample_nnz": sample},
+                   "nnz": nnz, "dims": list(cfg["dims"]), "rank": cfg["rank"],
+                   "sample_nnz": res["nnz"]},
         "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
                          "kind": "port", "sample": res["sample"]},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -551,9 +645,40 @@ def run_reference(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks through
+    torch.distributed.run on 127.0.0.1 (one process per GPU) and return its
+    exit code.  With FLYCOO_PG_BACKEND=gloo and fewer GPUs than ranks, ranks
+    share GPUs (functional runs only; host barriers, never a measurement)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ngpu = 0
+    if ngpu < args.gpus:
+        if env.get("FLYCOO_PG_BACKEND") != "gloo":
+            print(f"[bench] --gpus {args.gpus} but {ngpu} GPU(s) visible (set "
+                  "FLYCOO_PG_BACKEND=gloo for a functional run with shared GPUs)", file=sys.stderr)
+            return 2
+        env.setdefault("FLYCOO_PEER_SYNC", "host")  # ranks on one GPU never wait on each other
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if world != args.gpus:
+        sys.exit(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world, local)
     else:

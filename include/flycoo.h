@@ -11,7 +11,7 @@
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/modecycle):
  *   fc_mode_worker      <- _kernels.mode_worker            _kernels.py:38-88
- *                          fanned out by engine.mttkrp_mode engine.py:302-333
+ *                          fanned out by engine.mttkrp_mode engine.py:214-245
  *   fc_remap_cursor     <- _kernels.mode_worker cursor path _kernels.py:73-82
  *                          (+ _atomic_fetch_add             _kernels.py:18-35)
  *   fc_build_*          <- layout.build_sharded             layout.py:462-531
@@ -59,6 +59,11 @@ const char *fc_last_error(void);
  * shared memory; larger intervals accumulate in global memory (out rows). */
 int64_t fc_smem_acc_rows_max(int rank);
 int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
+/* Kernel variant for A/B runs (default 1, 1; the environment variables
+ * FLYCOO_PACK=0 / FLYCOO_PACK_WIDE=0 set it once when the library loads):
+ * pack = 8-byte sorted records for 3-mode tensors whose input coordinates
+ * fit 32 bits, pack_wide = the {c_w1, c_w2} + value variant otherwise. */
+int fc_set_kernel_variant(int pack, int pack_wide);
 /* Row capacity of a "direct" chunk merging consecutive small super-shards
  * (fast path only; returns m when merging is not supported). */
 int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);
@@ -91,7 +96,7 @@ int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);
  * size; multi-GPU: local part + send region, see dist.py).
  * `dims` (optional) lets 3-mode tensors whose two input coordinates fit 32
  * bits use 8-byte sorted records (same results, less shared traffic).
- * counters[0] += elements processed (the engine.py:335-338 check).        */
+ * counters[0] += elements processed (the engine.py:247-250 check).        */
 int fc_mode_worker(const void *src_crd, const float *src_val,
                    void *dst_crd, float *dst_val,
                    const float *const *factors, /* host array, N device ptrs */
@@ -165,6 +170,9 @@ int fc_gather_peer_rows(float *dst, const float *const *peer_src, const int64_t 
  * prior memory operations, or waits until (int32)(*flag - value) >= 0
  * (cuStreamWriteValue32 / cuStreamWaitValue32; no SM spins). */
 int fc_stream_signal(void *flag, uint32_t value, void *stream);
+/* 1 if fc_stream_wait flushes peers' remote writes on the current device
+ * (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES), 0 if not, <0 on error. */
+int fc_stream_wait_flush_supported(void);
 int fc_stream_wait(const void *flag, uint32_t value, void *stream);
 
 /* Cursor remap strategy (_kernels.py:73-80): b = src_sid[i, next_mode];

@@ -9,7 +9,8 @@ It restates the reference (``/root/reference/pkg/src/modecycle``) in numpy +
 the C kernel in ``flycoo_oracle.c``:
 
 * :func:`morton_interleave`   -- morton.py:15-44 (C)
-* :func:`canonical_build`     -- layout.py:462-531 (numpy; lexsort order,
+* :func:`canonical_build`     -- layout.py:462-531 (numpy + a C stable
+  radix sort for the lexsort orders when the composite key fits 64 bits;
   super-shard / shard geometry, shard ids, slot maps, mode-0 active buffer)
 * :func:`device_order`        -- the B200 layout's intra-shard order (this
   repo's design): same shard membership and offsets as the
@@ -73,6 +74,8 @@ def lib():
                 _f64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _i64p, _i64p,
                 ctypes.c_int, _i64p, _i64p, _i64p, ctypes.c_int, ctypes.c_int,
                 ctypes.c_int, _i64p]
+            L.orc_stable_sort_u64.restype = ctypes.c_int
+            L.orc_stable_sort_u64.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int, _i64p]
             L.orc_reference_mttkrp.restype = None
             L.orc_reference_mttkrp.argtypes = [
                 _i64p, _f64p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_f64p),
@@ -135,6 +138,32 @@ class CanonicalLayout:
         return int(self.subs.shape[1])
 
 
+def stable_order(key: np.ndarray, bits: int) -> np.ndarray:
+    """order = np.lexsort((seq, key)) for a uint64 key on bits [0, bits)
+    (C radix sort)."""
+    key = np.ascontiguousarray(key, dtype=np.uint64)
+    order = np.empty(key.shape[0], dtype=np.int64)
+    if lib().orc_stable_sort_u64(_p(key, _u64p), key.shape[0], int(bits), _p(order, _i64p)) != 0:
+        raise MemoryError("orc_stable_sort_u64")
+    return order
+
+
+def _lex_order(major: list, hi: np.ndarray, lo: np.ndarray, W: int) -> np.ndarray:
+    """np.lexsort((seq, lo, hi, *reversed(major))) -- `major` keys most
+    significant first, each given as (values, bit width) -- through one
+    composite-key radix sort when everything fits 64 bits."""
+    total = W + sum(b for _, b in major)
+    if total <= 64 and not (W > 64):
+        key = lo.astype(np.uint64, copy=True)
+        shift = W
+        for vals, b in reversed(major):
+            key |= np.asarray(vals, dtype=np.uint64) << np.uint64(shift)
+            shift += b
+        return stable_order(key, total)
+    seq = np.arange(lo.shape[0], dtype=np.int64)
+    return np.lexsort((seq, lo, hi) + tuple(v for v, _ in reversed(major)))
+
+
 def canonical_build(subs, vals, dims, m, k, g) -> CanonicalLayout:
     """layout.py:474-519 restated: iv = c // m; Morton (hi, lo) over all
     modes' interval coordinates; per mode lexsort by (iv_n, hi, lo, seq);
@@ -152,8 +181,9 @@ def canonical_build(subs, vals, dims, m, k, g) -> CanonicalLayout:
     seq = np.arange(nnz, dtype=np.int64)
     L = CanonicalLayout(tuple(int(d) for d in dims), m, k, g, subs, vals, iv, hi, lo)
     L.sids_all = np.empty((nnz, N), dtype=np.int64)
+    W = sum(int(x - 1).bit_length() for x in k)
     for n in range(N):
-        order = np.lexsort((seq, lo, hi, iv[:, n]))
+        order = _lex_order([(iv[:, n], int(k[n] - 1).bit_length())], hi, lo, W)
         pos = np.empty(nnz, dtype=np.int64)
         pos[order] = seq
         counts = np.bincount(iv[:, n], minlength=k[n]).astype(np.int64)
@@ -190,9 +220,13 @@ def device_order(L: CanonicalLayout) -> DeviceOrder:
     nnz, N = L.nnz, L.num_modes
     seq = np.arange(nnz, dtype=np.int64)
     orders, positions = [], []
+    W = sum(int(x - 1).bit_length() for x in L.k)
+    nsh = [int(L.ss_first_shard[n][-1]) for n in range(N)]
     for n in range(N):
         prev = (n - 1) % N
-        order = np.lexsort((seq, L.lo, L.hi, L.sids_all[:, prev], L.sids_all[:, n]))
+        order = _lex_order([(L.sids_all[:, n], max(nsh[n] - 1, 0).bit_length()),
+                            (L.sids_all[:, prev], max(nsh[prev] - 1, 0).bit_length())],
+                           L.hi, L.lo, W)
         pos = np.empty(nnz, dtype=np.int64)
         pos[order] = seq
         orders.append(order)
@@ -271,7 +305,7 @@ class OracleTensor:
 
     def set_workers(self, nu: int):
         """Static LPT schedule per mode (schedule.py:69-86) turned into
-        per-worker element ranges (engine.py:226-238)."""
+        per-worker element ranges (engine.py:138-150)."""
         L = self.L
         self.nu = int(nu)
         self.ranges = []
@@ -324,7 +358,7 @@ class OracleTensor:
         return out
 
     def sweep_all_modes(self, factors) -> list[np.ndarray]:
-        """engine.py:357-381: factor n replaced by its raw output after mode n."""
+        """engine.py:269-293: factor n replaced by its raw output after mode n."""
         working = list(factors)
         for n in range(self.L.num_modes):
             working[n] = self.mttkrp_mode(working, n)

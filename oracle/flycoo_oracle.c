@@ -9,12 +9,12 @@
  * What it restates (reference = /root/reference/pkg/src/modecycle):
  *   orc_morton          morton.py:15-44   (key_widths + interleave)
  *   orc_mode_worker     _kernels.py:38-88 (per-worker fused MTTKRP + remap)
- *   orc_mode_pass       engine.py:302-333 (fan-out of workers over threads,
+ *   orc_mode_pass       engine.py:214-245 (fan-out of workers over threads,
  *                                          join = end-of-mode barrier)
  *   orc_reference_mttkrp coo.py:406-426   (sequential oracle)
  *
  * Data layout is the reference's own: sids/idxs (nnz, N) int64 row-major,
- * vals (nnz,) float64, factors stacked row-wise (engine.py:241-248).
+ * vals (nnz,) float64, factors stacked row-wise (engine.py:153-160).
  * Build with -O2 -ffp-contract=off so every multiply and add rounds exactly
  * like numba/numpy do (no FMA contraction), which is what makes the oracle
  * bit-identical to the reference on the golden fixtures.
@@ -151,7 +151,7 @@ static void *orc_worker_run(void *arg) {
   return NULL;
 }
 
-/* engine.py:302-341: one call = one pass (compute and/or remap) over every
+/* engine.py:214-253: one call = one pass (compute and/or remap) over every
  * worker's ranges; worker w owns ranges [range_offs[w], range_offs[w+1]).
  * Returns total processed elements; *errflag_out = overflowed shard + 1. */
 int64_t orc_mode_pass(const int64_t *sids, const int64_t *idxs, const double *vals,
@@ -216,4 +216,41 @@ void orc_reference_mttkrp(const int64_t *subs, const double *vals, int64_t nnz,
     for (int64_t r = 0; r < rank; ++r) orow[r] += ell[r] * vals[i];
   }
   free(ell);
+}
+
+/* ------------------------------------------------------------ stable sort */
+
+/* Stable LSD radix sort of `keys` on bits [0, bits): order[r] = index of the
+ * r-th smallest key, equal keys in index order -- i.e. np.lexsort((seq, key))
+ * for a composite key.  canonical_build uses it for the per-mode orders
+ * lexsort((seq, lo, hi, iv_n)) of layout.py:484 when (iv_n, hi, lo) packs into
+ * 64 bits, which turns the 76.9M-element c2 build from minutes into seconds.
+ * Returns 0, or -1 when out of memory. */
+int orc_stable_sort_u64(const uint64_t *keys, int64_t n, int bits, int64_t *order) {
+  enum { D = 11, B = 1 << D };
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  if (n < 2 || bits <= 0) return 0;
+  int64_t *tmp = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  uint64_t *kc = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  uint64_t *kt = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  if (!tmp || !kc || !kt) {
+    free(tmp); free(kc); free(kt);
+    return -1;
+  }
+  memcpy(kc, keys, (size_t)n * sizeof(uint64_t));
+  int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (B + 1));
+  for (int shift = 0; shift < bits; shift += D) {
+    memset(cnt, 0, sizeof(int64_t) * (B + 1));
+    for (int64_t i = 0; i < n; ++i) cnt[((kc[i] >> shift) & (B - 1)) + 1]++;
+    for (int d = 0; d < B; ++d) cnt[d + 1] += cnt[d];
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t dst = cnt[(kc[i] >> shift) & (B - 1)]++;
+      tmp[dst] = order[i];
+      kt[dst] = kc[i];
+    }
+    memcpy(order, tmp, (size_t)n * sizeof(int64_t));
+    uint64_t *sw = kc; kc = kt; kt = sw;
+  }
+  free(cnt); free(tmp); free(kc); free(kt);
+  return 0;
 }

@@ -8,17 +8,19 @@ CUDA kernels (libflycoo.so, C ABI in include/flycoo.h).
 
 from .engine import (REMAP_STRATEGIES, BufferOrderError, RemapCursors, ShardOverflowError,
                      TrafficCounters, mttkrp_mode, remap_store, sweep_all_modes)
+from .coo import CooTensor, Element
 from .factors import DeviceFactorSet
-from .layout import (DeviceShardedTensor, PartitionPlan, build_device_sharded, plan_from_counts,
-                     record_bytes)
+from .layout import (CheckResult, DeviceShardedTensor, PartitionPlan, PlanReport,
+                     build_device_sharded, build_sharded, device_has_duplicates, plan_from_counts,
+                     record_bytes, validate_plan)
 from .params import (InfeasibleParamsError, PartitionParams, default_element_bytes,
                      device_params, element_size_bits, select_params)
 from .schedule import ScheduleMap, load_stats, schedule_super_shards
 from .cpals import CpalsConfig, CpalsResult, cp_als, fit, normalize_factors
 
-# reference-compatible aliases
+# reference-compatible names (FactorSet.random reproduces the reference's
+# Philox stream; build_sharded takes the reference's (tensor, params))
 FactorSet = DeviceFactorSet
 ShardedTensor = DeviceShardedTensor
-build_sharded = build_device_sharded
 
 __version__ = "0.1.0"

@@ -31,6 +31,7 @@ _SIGS = {
     "fc_value_embedded": (_int, [_int]),
     "fc_smem_acc_rows_max": (_i64, [_int]),
     "fc_tile_elems": (_int, []),
+    "fc_set_kernel_variant": (_int, [_int, _int]),
     "fc_chunk_rows_max": (_i64, [_int, _int, _i64]),
     "fc_mode_worker": (_int, [
         _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val
@@ -66,6 +67,7 @@ _SIGS = {
     "fc_gather_peer_rows": (_int, [_vp, _vp, _vp, _int, _int, _i64, _vp]),
     "fc_stream_signal": (_int, [_vp, _c.c_uint32, _vp]),
     "fc_stream_wait": (_int, [_vp, _c.c_uint32, _vp]),
+    "fc_stream_wait_flush_supported": (_int, []),
     "fc_remap_cursor": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _i64, _vp, _vp, _vp, _vp]),
     "fc_scatter_records": (_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _int, _vp, _vp, _vp]),
     "fc_build_morton": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp]),

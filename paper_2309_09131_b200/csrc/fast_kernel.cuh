@@ -40,9 +40,6 @@ constexpr int kFWarps = kFBlock / 32;
 constexpr int kFIPT = FAST_IPT;
 constexpr int kFTile = kFBlock * kFIPT;
 
-#ifdef FAST_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[5];
-#endif
 
 template <int NM, int LPG>
 struct FastPlan {
@@ -85,12 +82,8 @@ __device__ __forceinline__ void element_prod(const ModeArgs &a, int R, int col, 
   for (int w = 0; w < NM; ++w) {
     if (w == MODE) continue;
     const int c = w == 0 ? q.x : w == 1 ? q.y : w == 2 ? q.z : q.w;
-#ifdef FAST_NO_GATHER  // experiment only: no factor loads
-    const float4 f = make_float4(__int_as_float(c), 1.f, 1.f, 1.f);
-#else
     const float *F = a.fac[w] + (uint64_t)(uint32_t)c * (uint32_t)(RT > 0 ? RT : R) + col;
     const float4 f = __ldg(reinterpret_cast<const float4 *>(F));
-#endif
     if (first) {
       pr[0] = f.x; pr[1] = f.y; pr[2] = f.z; pr[3] = f.w;
       first = false;
@@ -204,13 +197,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     return (lr >= 0 && lr < rows) ? lr : -1;
   };
 
-#ifdef FAST_PHASE_TIMING
-  unsigned long long ph_acc[5] = {0, 0, 0, 0, 0};
-  long long ph_t = clock64();
-#define FAST_PROBE(k) do { if (tid == 0) { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } } while (0)
-#else
-#define FAST_PROBE(k) do { } while (0)
-#endif
   for (int64_t t0 = start; t0 < end; t0 += kFTile) {
     const int cnt = (int)min64(kFTile, end - t0);
     // ---------------------------------------------------------------- A
@@ -253,18 +239,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     }
     __syncwarp();
     // ---------------------------------------------------------------- B
-#ifdef FAST_NO_SORT  // experiment only: records stay in tile order
-    {
-#pragma unroll
-      for (int j = 0; j < kFIPT; ++j) {
-        const int e = j * kFBlock + tid;
-        if (e < cnt) s_sorted[e + e / P] = rec[j];
-      }
-      if (tid == 0) s_misc[kFWarps] = cnt;
-      __syncthreads();
-    }
-    if (false)
-#endif
     {
     // B1: warp-local ranks.  The rank is parked in the record's mode word
     // as (rank << 8 | local row) until B3 restores the coordinate -- keeps
@@ -319,7 +293,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
-    FAST_PROBE(0);
     {
       int tot = 0;
       if (tid < rows) {
@@ -353,7 +326,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       }
     }
     __syncthreads();
-    FAST_PROBE(1);
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int x = comp<MODE>(rec[j]);
@@ -366,7 +338,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       }
     }
     __syncthreads();
-    FAST_PROBE(2);
     }
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
@@ -383,11 +354,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       s_bnd_row[2 * gi + 1] = -1;
     }
     const int pb = gi * P;
-#ifdef FAST_NO_C  // experiment only
-    const int pe = pb;
-#else
     const int pe = min(pb + P, nvalid);
-#endif
     if (pb < pe) {
       int cur = comp<MODE>(s_sorted[phys(pb)]);
       bool head = pb > 0 && comp<MODE>(s_sorted[phys(pb - 1)]) == cur;
@@ -425,43 +392,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       const float *svp = s_sval + gi;
       const FacBases<NM, MODE> fb(a, RT > 0 ? RT : R, col);
       int p = pb;
-#ifdef FAST_SWP
-      // software pipeline (distance 1): block b+1's record loads and gathers
-      // are issued before block b is consumed
-      if (p + U <= pe) {
-        int4 qa[U], qb[U];
-        float va[U], vb[U];
-        float pa[U][4], pb_[U][4];
-        auto fetch = [&](int at, int4 (&q)[U], float (&vv)[U], float (&pr)[U][4]) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            q[u] = sp[at + u];
-            vv[u] = EMB ? __int_as_float(q[u].w) : svp[at + u];
-          }
-          if (col_ok) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) element_prod(fb, q[u], pr[u]);
-          }
-        };
-        fetch(p, qa, va, pa);
-        p += U;
-        while (true) {
-          const bool more = p + U <= pe;
-          if (more) fetch(p, qb, vb, pb_);
-#pragma unroll
-          for (int u = 0; u < U; ++u) consume(comp<MODE>(qa[u]), va[u], pa[u]);
-          if (!more) break;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            qa[u] = qb[u];
-            va[u] = vb[u];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) pa[u][k] = pb_[u][k];
-          }
-          p += U;
-        }
-      }
-#else
       for (; p + U <= pe; p += U) {
         int4 q[U];
         float vv[U];
@@ -478,7 +408,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
 #pragma unroll
         for (int u = 0; u < U; ++u) consume(comp<MODE>(q[u]), vv[u], pr[u]);
       }
-#endif
       for (; p < pe; ++p) {
         const int4 q = sp[p];
         const float vv = EMB ? __int_as_float(q.w) : svp[p];
@@ -495,7 +424,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       }
     }
     __syncthreads();
-    FAST_PROBE(3);
     // ---------------------------------------------------------------- D
     // a row crossing pieces a..b: tail(a) + head(a+1) + ... + head(b), in
     // piece order (see pack_kernel.cuh)
@@ -516,7 +444,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         }
       }
     }
-    FAST_PROBE(4);
   }
   if (!direct) {
     __syncthreads();
@@ -527,10 +454,6 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
   }
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
-#ifdef FAST_PHASE_TIMING
-  if (tid == 0)
-    for (int k = 0; k < 5; ++k) atomicAdd(&g_phase_cycles[k], ph_acc[k]);
-#endif
 }
 
 template <int NM, int MODE, int LPG, int RT, bool PEER = false>

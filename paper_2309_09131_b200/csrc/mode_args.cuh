@@ -230,4 +230,13 @@ int fast_dispatch_peer_n2(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 int fast_dispatch_peer_n3(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 int fast_dispatch_peer_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 
+// Kernel-variant switches, fixed when the library loads (FLYCOO_PACK=0 /
+// FLYCOO_PACK_WIDE=0 in the environment, for A/B runs) or set through
+// fc_set_kernel_variant(); never read from the environment on the launch path.
+struct KernelVariant {
+  bool pack = true;
+  bool pack_wide = true;
+};
+KernelVariant &kernel_variant();
+
 }  // namespace fc

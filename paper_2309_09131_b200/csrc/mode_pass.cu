@@ -3,7 +3,7 @@
 //
 // Replaces the reference's per-thread numba kernel _kernels.mode_worker
 // (/root/reference/pkg/src/modecycle/_kernels.py:38-88) and the thread
-// fan-out / join of engine.mttkrp_mode (engine.py:302-333).
+// fan-out / join of engine.mttkrp_mode (engine.py:214-245).
 //
 // Work decomposition: one CTA per chunk, a chunk being a
 // contiguous run of elements inside ONE super-shard, so the CTA owns (or
@@ -27,6 +27,8 @@
 // bitwise reproducible.  Rows of super-shards split over several chunks
 // are summed by K2 in chunk order.
 #include <cub/block/block_radix_sort.cuh>
+#include <stdlib.h>
+#include <string.h>
 
 #include "mode_args.cuh"
 
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(256) reduce_level_kernel(const int64_t *tasks,
   else slots[dst * cells + idx] = s;
 }
 
-// Remap-only pass (split_remap second pass, engine.py:312) of n elements;
+// Remap-only pass (split_remap second pass, engine.py:224) of n elements;
 // also the receiver unpack of the NCCL exchange (fc_scatter_records).
 template <int CW4, bool EMB>
 __global__ void __launch_bounds__(256) remap_only_kernel(const __grid_constant__ ModeArgs a, int64_t n) {
@@ -469,6 +471,18 @@ int dispatch(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
 
 int64_t smem_acc_rows_max(int rank) { return rank > 0 ? kSmemAccBytes / (4 * (int64_t)rank) : 0; }
 
+// read once, when the library is loaded (dispatch.cuh)
+static KernelVariant variant_from_env() {
+  KernelVariant v;
+  const char *p = getenv("FLYCOO_PACK");
+  const char *w = getenv("FLYCOO_PACK_WIDE");
+  v.pack = !(p && strcmp(p, "0") == 0);
+  v.pack_wide = !(w && strcmp(w, "0") == 0);
+  return v;
+}
+static KernelVariant g_variant = variant_from_env();
+KernelVariant &kernel_variant() { return g_variant; }
+
 }  // namespace fc
 
 using namespace fc;
@@ -476,6 +490,12 @@ using namespace fc;
 extern "C" {
 
 int64_t fc_smem_acc_rows_max(int rank) { return fc::smem_acc_rows_max(rank); }
+
+int fc_set_kernel_variant(int pack, int pack_wide) {
+  fc::kernel_variant().pack = pack != 0;
+  fc::kernel_variant().pack_wide = pack_wide != 0;
+  return FC_OK;
+}
 int fc_tile_elems(void) { return kTile; }
 
 // Row capacity of a direct chunk (several whole super-shards in at most one

@@ -76,13 +76,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-#ifdef FAST_PHASE_TIMING
-  unsigned long long ph_acc[5] = {0, 0, 0, 0, 0};
-  long long ph_t = clock64();
-#define PACK_PROBE(k) do { if (tid == 0) { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } } while (0)
-#else
-#define PACK_PROBE(k) do { } while (0)
-#endif
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t chunk = blockIdx.x;
   const int64_t start = a.chunk_start[chunk];
@@ -158,13 +151,9 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (bad) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
     }
     __syncwarp();
-    PACK_PROBE(0);
     // ---------------------------------------------------------------- B
     int *wh = s_hist + warp * hstride;
-#ifndef PACK_LANE_ROWS
-#define PACK_LANE_ROWS 1
-#endif
-    if (PACK_LANE_ROWS && hist_rows32) {
+    if (hist_rows32) {
       // <= 32 rows: lane r owns row r's count in this warp.  From the key-bit
       // ballots lane r forms `own` = the lanes holding row r; an element's
       // equal-row peers and its group's base are then one shuffle each from
@@ -226,7 +215,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     }
     }
     __syncthreads();
-    PACK_PROBE(1);
     {
       int tot = 0;
       if (tid < rows) {
@@ -268,7 +256,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(2);
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int x = comp<MODE>(rec[j]);
@@ -285,7 +272,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(3);
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
     if (tid == 0 && t0 + kFTile < end) {
@@ -392,7 +378,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       }
     }
     __syncthreads();
-    PACK_PROBE(4);
     // ---------------------------------------------------------------- D
     // A row that crosses pieces a..b left a tail entry in piece a and a head
     // entry in each of a+1..b; its sum is tail(a) + head(a+1) + ... + head(b)
@@ -425,10 +410,6 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     for (int i = tid; i < n4; i += kFBlock) d4[i] = s4[i];
   }
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
-#ifdef FAST_PHASE_TIMING
-  if (tid == 0)
-    for (int k = 0; k < 5; ++k) atomicAdd(&g_phase_cycles[k], ph_acc[k]);
-#endif
 }
 
 template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>

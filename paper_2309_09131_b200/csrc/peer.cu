@@ -41,6 +41,37 @@ StreamValueFn driver_fn(const char *name) {
     return nullptr;
   return reinterpret_cast<StreamValueFn>(fn);
 }
+
+// Whether the current device can flush remote (NVLink) writes ahead of a
+// stream wait (CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES), queried once per
+// device -- a query, not a stream operation, so it is also safe while the
+// stream is being captured into a graph.  -1 on a query failure.
+int can_flush_remote_writes() {
+  typedef CUresult (*AttrFn)(int *, CUdevice_attribute, CUdevice);
+  static AttrFn attr = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuDeviceGetAttribute", &fn, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return (AttrFn) nullptr;
+    return reinterpret_cast<AttrFn>(fn);
+  }();
+  static int cached[64];
+  static bool init = [] {
+    for (int &c : cached) c = -2;
+    return true;
+  }();
+  (void)init;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || !attr) return -1;
+  if (cached[dev] == -2) {
+    int v = 0;
+    cached[dev] = attr(&v, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, (CUdevice)dev) == CUDA_SUCCESS
+                      ? (v != 0)
+                      : -1;
+  }
+  return cached[dev];
+}
 }  // namespace
 
 extern "C" {
@@ -132,6 +163,8 @@ int fc_stream_signal(void *flag, uint32_t value, void *stream) {
   return FC_OK;
 }
 
+int fc_stream_wait_flush_supported(void) { return can_flush_remote_writes(); }
+
 int fc_stream_wait(const void *flag, uint32_t value, void *stream) {
   static StreamValueFn fn = driver_fn("cuStreamWaitValue32");
   FC_CHECK_ARG(flag, "null flag");
@@ -139,19 +172,17 @@ int fc_stream_wait(const void *flag, uint32_t value, void *stream) {
     set_error("cuStreamWaitValue32 unavailable");
     return FC_ERR_CUDA;
   }
-  // FLUSH: the peers' NVLink stores that precede their flag write are visible
-  // to this stream's later kernels (devices without remote-write flushing
-  // reject the flag: plain GEQ wait, remembered)
-  static int flush_ok = 1;
-  CUresult r = CUDA_ERROR_INVALID_VALUE;
-  if (flush_ok) {
-    r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)),
-           value, CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH);
-    if (r == CUDA_ERROR_INVALID_VALUE || r == CUDA_ERROR_NOT_SUPPORTED) flush_ok = 0;
+  // FLUSH (devices that support it, per the device attribute): the peers'
+  // NVLink stores that precede their flag write are visible to this stream's
+  // later kernels.  Any failure of the wait itself is an error.
+  const int flush = can_flush_remote_writes();
+  if (flush < 0) {
+    set_error("cuDeviceGetAttribute(CAN_FLUSH_REMOTE_WRITES) failed");
+    return FC_ERR_CUDA;
   }
-  if (!flush_ok)
-    r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)),
-           value, CU_STREAM_WAIT_VALUE_GEQ);
+  const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream),
+                        reinterpret_cast<CUdeviceptr>(const_cast<void *>(flag)), value, flags);
   if (r != CUDA_SUCCESS) {
     set_error("cuStreamWaitValue32 failed (%d)", (int)r);
     return FC_ERR_CUDA;

@@ -40,7 +40,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .layout import DeviceShardedTensor, PartitionPlan, default_chunk_elems, make_mode_work
+from .layout import DeviceShardedTensor, PartitionPlan, make_mode_work, plan_chunk_elems
 
 __all__ = ["partition_super_shards", "RankModePlan", "build_rank_plans", "DistShardedTensor",
            "CudaOps", "dist_sweep_all_modes"]
@@ -196,7 +196,7 @@ class DistShardedTensor:
             # same chunking as the single-GPU plan -> bitwise-identical sums
             p = self.plans[mode]
             self._work[key] = make_mode_work(lp, mode, rank_r, self.device,
-                                             chunk_elems=default_chunk_elems(self.plan.nnz),
+                                             chunk_elems=plan_chunk_elems(self.plan, mode, rank_r),
                                              ss_range=(p.ss_lo, p.ss_hi))
         return self._work[key]
 

@@ -1,8 +1,8 @@
 """Drop-in engine: mttkrp_mode / sweep_all_modes / remap_store on the B200.
 
 Same signatures, preconditions, exceptions and counters as the reference
-engine (/root/reference/pkg/src/modecycle/engine.py:28-381).  The per-thread
-numba kernel and its thread fan-out (engine.py:302-333, _kernels.py:38-88)
+engine (/root/reference/pkg/src/modecycle/engine.py:28-293).  The per-thread
+numba kernel and its thread fan-out (engine.py:214-245, _kernels.py:38-88)
 become one stream-ordered call of ``fc_mode_worker`` (libflycoo, sm_100a),
 whose CTAs own super-shard chunks.  There is no CPU path: the CUDA library
 must be present.
@@ -12,7 +12,7 @@ Differences a caller can see, each forced by the device:
   :class:`~.factors.DeviceFactorSet` (host FactorSet-likes are converted),
   outputs are fp32 CUDA tensors of shape (I_mode, R);
 * ``workers`` is validated but the GPU decomposition ignores it, and the
-  ScheduleMap is validated (engine.py:274-277) but its assignment unused;
+  ScheduleMap is validated (engine.py:186-189) but its assignment unused;
 * ``sweep_all_modes`` runs every mode back to back on the stream and checks
   the processed counts and device error flags once at the end (one host
   sync per sweep instead of one per mode); ``mode_seconds`` gets per-mode
@@ -50,7 +50,7 @@ class BufferOrderError(ValueError):
 
 @dataclass
 class TrafficCounters:
-    """Model data-volume counters per mode, closed forms of engine.py:137-179
+    """Model data-volume counters per mode, closed forms of engine.py:49-91
     (tensor read + rewritten once, N-1 rank-R factor rows gathered and one
     output row updated per element; factor entries counted at 8 bytes as in
     the reference model)."""
@@ -89,7 +89,7 @@ class TrafficCounters:
 
 @dataclass
 class RemapCursors:
-    """Fill records of the upcoming mode's shards (engine.py:182-209)."""
+    """Fill records of the upcoming mode's shards (engine.py:94-121)."""
 
     base: np.ndarray
     fills: np.ndarray
@@ -131,7 +131,7 @@ def _ensure_sids(st: DeviceShardedTensor) -> None:
 def remap_store(element_row: int, next_mode: int, cursors: RemapCursors,
                 st: DeviceShardedTensor) -> int:
     """Store one active element into its next-mode shard slot; returns the
-    slot (engine.py:212-223, single-element mirror of the kernel remap)."""
+    slot (engine.py:124-135, single-element mirror of the kernel remap)."""
     _ensure_sids(st)
     a, b = st.active, 1 - st.active
     shard = int(st._sids[a][element_row, next_mode])
@@ -154,7 +154,7 @@ def _coerce_factors(factors, device) -> DeviceFactorSet:
 
 
 def check_errors(st: DeviceShardedTensor, next_mode: int | None = None) -> None:
-    """Host check of the deferred device counters (engine.py:335-351)."""
+    """Host check of the deferred device counters (engine.py:247-263)."""
     stat = st._stat.cpu()
     processed = int(stat[0])
     flags = int(stat[1]) & 0xFFFFFFFF
@@ -175,7 +175,7 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
                 split_remap: bool = False, alloc_log: dict | None = None, *,
                 check: bool = True) -> torch.Tensor:
     """Output factor for `mode`; leaves the tensor ordered for mode
-    (mode + 1) % N (engine.py:251-354).  For a fixed active order the result
+    (mode + 1) % N (engine.py:163-266).  For a fixed active order the result
     is bitwise reproducible (fixed-order sums, no data atomics)."""
     plan, params = st.plan, st.params
     nmodes = st.num_modes
@@ -265,7 +265,7 @@ def sweep_all_modes(st: DeviceShardedTensor, factors, smap, workers: int | None 
                     remap: str = "slot", counters: TrafficCounters | None = None,
                     mode_seconds: list | None = None, split_remap: bool = False) -> DeviceFactorSet:
     """One pass over every mode, each factor overwritten by its raw MTTKRP
-    output right after its mode (engine.py:357-381)."""
+    output right after its mode (engine.py:269-293)."""
     factors = _coerce_factors(factors, st.device)
     working = list(factors.factors)
     lambdas = factors.lambdas.copy()

@@ -89,7 +89,19 @@ class DeviceFactorSet:
 
     @classmethod
     def random(cls, dims, rank: int, seed: int, device="cuda") -> "DeviceFactorSet":
-        """U(0,1) fp32 entries from Philox4x32-10 (stream = mode), on device."""
+        """The reference's ``FactorSet.random`` (coo.py:184-192): U[0,1)
+        float64 entries from ``np.random.Generator(np.random.Philox(seed))``,
+        drawn mode by mode in the same order, then held as fp32 on the device
+        -- the fp32 rounding of the reference's factors for the same seed."""
+        rng = np.random.Generator(np.random.Philox(seed))
+        return cls(tuple(rng.random((int(d), rank)).astype(np.float32) for d in dims), None, device,
+                   validate=False)
+
+    @classmethod
+    def random_device(cls, dims, rank: int, seed: int, device="cuda") -> "DeviceFactorSet":
+        """U(0,1) fp32 entries from Philox4x32-10 (stream = mode) generated on
+        the device (the billion-row factors of c3/c4 without a host round
+        trip).  Not the reference's stream: use :meth:`random` for that."""
         dev = torch.device(device)
         fs = []
         for w, d in enumerate(dims):

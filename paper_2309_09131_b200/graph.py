@@ -13,7 +13,7 @@ and makes small tensors launch-bound no more.
 The device checks of the eager engine are kept: the graph zeroes the
 [processed, flags] counters first, and :meth:`SweepGraph.run` reads them
 after the replay and raises ShardOverflowError / BufferOrderError /
-RuntimeError exactly as engine.check_errors does (engine.py:335-351).
+RuntimeError exactly as engine.check_errors does (engine.py:247-263).
 Slot remap only (the cursor strategy needs a host check per mode).
 """
 
@@ -126,6 +126,7 @@ class SweepGraph:
         g.replay()
         # host state of N swaps; the device counters were zeroed by the graph
         st.active = st.active ^ (self.N % 2)
+        st._back_mode = self.N - 1  # the last pass read mode N-1's arrangement
         st._expected = self.N * st.nnz
         check_errors(st)  # synchronizes: the host outputs are complete too
         return outs

@@ -35,8 +35,8 @@ import torch
 from . import _lib
 from .params import PartitionParams
 
-__all__ = ["PartitionPlan", "DeviceShardedTensor", "build_device_sharded", "plan_from_counts",
-           "record_bytes", "ModeWork"]
+__all__ = ["PartitionPlan", "DeviceShardedTensor", "build_sharded", "build_device_sharded",
+           "plan_from_counts", "record_bytes", "ModeWork", "device_has_duplicates"]
 
 
 def record_bytes(nmodes: int) -> int:
@@ -152,6 +152,9 @@ def reduce_plan(nch: np.ndarray, part_base: np.ndarray, fan: int = REDUCE_FAN):
     return r1, r2, slot
 
 
+BIG_SS_AVG = 400_000  # super-shards averaging this many nonzeros get 32k-element chunks
+
+
 def default_chunk_elems(nnz: int, tile: int = 2048, avg_ss: float = 0.0) -> int:
     """Chunk size: 8192 elements, smaller for small tensors so that every
     SM gets work (multiples of the 2048-element tile); 32768 for modes whose
@@ -159,7 +162,7 @@ def default_chunk_elems(nnz: int, tile: int = 2048, avg_ss: float = 0.0) -> int:
     to write and reduce, 45.8 -> 44.9 ms at 1B nonzeros; c2 and c4 are
     neutral or slower with larger chunks and stay below the threshold)."""
     env = os.environ.get("FLYCOO_CHUNK")
-    cap = int(env) if env else (32768 if avg_ss >= 400_000 else 8192)
+    cap = int(env) if env else (32768 if avg_ss >= BIG_SS_AVG else 8192)
     want = _cdiv(max(int(nnz), 1), 148 * 4)
     return int(min(cap, max(tile, _cdiv(want, tile) * tile)))
 
@@ -189,6 +192,24 @@ def direct_groups(counts: np.ndarray, tile: int, group: int):
         nss.append(j - i)
         i = j
     return np.asarray(first, dtype=np.int64), np.asarray(nss, dtype=np.int64)
+
+
+def plan_chunk_elems(plan: PartitionPlan, mode: int, rank: int, merge: bool = True) -> int:
+    """The chunk size :func:`make_mode_work` picks for the whole-tensor plan
+    of `mode` -- what a partitioned sweep passes for its slices so that its
+    chunks, partial tiles and sums are the single-GPU ones."""
+    L = _lib.load()
+    m = int(plan.params.m[mode])
+    k = int(np.asarray(plan.ss_counts[mode]).shape[0])
+    nnz = plan.nnz
+    tile = int(L.fc_tile_elems())
+    smem = m <= int(L.fc_smem_acc_rows_max(int(rank)))
+    sparse = nnz < tile * max(k, 1)
+    rows_cap = int(L.fc_chunk_rows_max(plan.num_modes, int(rank), m)) if smem else m
+    if smem and merge and sparse and rows_cap // m > 1:
+        return default_chunk_elems(nnz, tile)
+    # (3-mode tensors only: c3's 4-mode tile kernel was slower with 32k chunks)
+    return default_chunk_elems(nnz, tile, avg_ss=nnz / max(k, 1) if plan.num_modes == 3 else 0.0)
 
 
 def make_mode_work(plan: PartitionPlan, mode: int, rank: int, device, chunk_elems: int | None = None,
@@ -306,6 +327,8 @@ class DeviceShardedTensor:
         self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._expected = 0
         self._sids = None           # per-element shard ids, only for the cursor strategy
+        self._back_mode = None      # mode whose order the back buffer holds (None: unwritten)
+        self.build_stages = {}      # build stage -> seconds (CUDA events), set by the builders
 
     # --------------------------------------------------------------- props
     @property
@@ -325,6 +348,7 @@ class DeviceShardedTensor:
         return record_bytes(self.num_modes)
 
     def swap(self, new_mode: int, still_canonical: bool) -> None:
+        self._back_mode = self.active_mode
         self.active = 1 - self.active
         self.active_mode = new_mode
         self.canonical = self.canonical and still_canonical
@@ -350,26 +374,33 @@ class DeviceShardedTensor:
             v = val.cpu().numpy().astype(np.float64)
         return c, v
 
-    def positions_in_mode(self, mode: int) -> torch.Tensor:
-        """Mode-`mode` buffer position of every element of the active buffer
-        (composition of slot maps; needs the canonical arrangement)."""
+    def positions_in_mode(self, mode: int, from_mode: int | None = None) -> torch.Tensor:
+        """Mode-`mode` buffer position of every element of a buffer ordered
+        for `from_mode` (default: the active buffer) -- composition of slot
+        maps; needs the canonical arrangement."""
         if not self.canonical:
             raise ValueError("positions are only defined for the canonical arrangement")
         N = self.num_modes
         pos = torch.arange(self.nnz, device=self.device, dtype=torch.int64)
-        n = self.active_mode
+        n = self.active_mode if from_mode is None else from_mode
         while n != mode:
             pos = (self.slot_maps[n].to(torch.int64) & 0xFFFFFFFF)[pos]
             n = (n + 1) % N
         return pos
 
-    def shard_ids(self) -> np.ndarray:
-        """(nnz, N) int64 shard id per mode of the active buffer's elements."""
+    def shard_ids(self, which: int | None = None) -> np.ndarray:
+        """(nnz, N) int64 shard id per mode of a buffer's elements (default:
+        the active buffer; zeros for a back buffer no pass has written yet,
+        like the reference's freshly built back buffer, layout.py:526-528)."""
+        b = self.active if which is None else which
         if self._sids is not None:
-            return self._sids[self.active].to(torch.int64).cpu().numpy()
-        out = np.empty((self.nnz, self.num_modes), dtype=np.int64)
+            return self._sids[b].to(torch.int64).cpu().numpy()
+        from_mode = self.active_mode if b == self.active else self._back_mode
+        out = np.zeros((self.nnz, self.num_modes), dtype=np.int64)
+        if from_mode is None:
+            return out
         for w in range(self.num_modes):
-            pos = self.positions_in_mode(w).cpu().numpy()
+            pos = self.positions_in_mode(w, from_mode).cpu().numpy()
             out[:, w] = np.searchsorted(self.plan.shard_offsets[w], pos, side="right") - 1
         return out
 
@@ -380,9 +411,22 @@ class DeviceShardedTensor:
         c, v = self._host_coords_vals(self.active)
         return self.shard_ids(), c, v
 
-    def to_coo(self):
+    def back_arrays(self):
+        """(sids, idxs, vals) of the back buffer (layout.py:423-425): the
+        previous mode's arrangement after a pass, zeros before the first."""
+        b = 1 - self.active
+        if self._back_mode is None and self._sids is None:
+            z = np.zeros((self.nnz, self.num_modes), dtype=np.int64)
+            return z, z.copy(), np.zeros(self.nnz)
+        c, v = self._host_coords_vals(b)
+        return self.shard_ids(b), c, v
+
+    def to_coo(self, dims=None):
+        """The active buffer as a validated :class:`~.coo.CooTensor`
+        (layout.py:432-434)."""
+        from .coo import CooTensor
         c, v = self._host_coords_vals(self.active)
-        return c, v
+        return CooTensor(tuple(dims or self.params.dims), c, v)
 
     def accounting(self) -> dict:
         plan_aux = sum(a.size for g in (self.plan.ss_counts, self.plan.ss_elem_offsets,
@@ -419,10 +463,114 @@ def _bitlen(x: int) -> int:
     return int(x).bit_length()
 
 
-def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> DeviceShardedTensor:
+_MIX1 = -7046029254386353131   # 0x9E3779B97F4A7C15 as int64 (splitmix64 constants)
+_MIX2 = -4658895280553007687   # 0xBF58476D1CE4E5B9
+_MIX3 = -7723592293110705685   # 0x94D049BB133111EB
+
+
+def _mix64(x: torch.Tensor) -> torch.Tensor:
+    """splitmix64 finaliser on int64 tensors (two's-complement wrap-around;
+    logical shifts emulated with masks)."""
+    x = x * _MIX2
+    x = x ^ ((x >> 30) & ((1 << 34) - 1))
+    x = x * _MIX3
+    return x ^ ((x >> 31) & ((1 << 33) - 1))
+
+
+def device_has_duplicates(coords: torch.Tensor, dims, buckets: int | None = None) -> bool:
+    """True iff two rows of the (nnz, N) integer coordinate tensor are equal
+    -- the reference's "duplicate coordinates" check (coo.py:88-89), run
+    where the coordinates live.  Rows are keyed by their row-major flattened
+    index when prod(dims) fits 63 bits (exact), else by a 64-bit hash whose
+    equal-hash groups are compared coordinate by coordinate; the keys are
+    sorted in hash buckets so the sort scratch stays ~nnz/buckets * 24 B."""
+    nnz, N = int(coords.shape[0]), int(coords.shape[1])
+    if nnz < 2:
+        return False
+    dims = [int(d) for d in dims]
+    exact = int(np.prod(np.asarray(dims, dtype=object))) < (1 << 63)
+    key = torch.zeros(nnz, dtype=torch.int64, device=coords.device)
+    for n in range(N):
+        c = coords[:, n].to(torch.int64)
+        if exact:
+            key.mul_(dims[n]).add_(c)
+        else:
+            salt = (((n + 1) * _MIX1 + (1 << 63)) % (1 << 64)) - (1 << 63)  # wrapped to int64
+            key = _mix64(key ^ _mix64(c + salt))
+    if buckets is None:
+        buckets = max(1, min(16, -(-nnz // (1 << 28))))
+    bsel = _mix64(key) & (buckets - 1) if buckets > 1 and (buckets & (buckets - 1)) == 0 else None
+    if buckets > 1 and bsel is None:
+        raise ValueError("buckets must be a power of two")
+    for b in range(buckets):
+        idx = torch.arange(nnz, device=key.device) if bsel is None else torch.nonzero(bsel == b).squeeze(1)
+        if idx.numel() < 2:
+            continue
+        kv, perm = torch.sort(key[idx])
+        eq = kv[1:] == kv[:-1]
+        if not bool(eq.any()):
+            continue
+        if exact:
+            return True
+        # hash collisions or true duplicates: compare the rows of every
+        # equal-hash group exactly (on the host; groups are tiny)
+        at = torch.nonzero(eq).squeeze(1)
+        members = torch.unique(torch.cat([at, at + 1]))
+        rows = idx[perm[members]]
+        sub = coords[rows].to(torch.int64).cpu().numpy()
+        hk = kv[members].cpu().numpy()
+        for h in np.unique(hk):
+            grp = sub[hk == h]
+            if len(np.unique(grp, axis=0)) != len(grp):
+                return True
+    return False
+
+
+class _StageClock:
+    """CUDA-event timestamps between build stages (PAPER.md:762 reports the
+    super-shard generation, Morton ordering and shard generation stages)."""
+
+    def __init__(self):
+        self.marks = [("start", torch.cuda.Event(enable_timing=True))]
+        self.marks[0][1].record()
+
+    def mark(self, name: str):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.marks.append((name, e))
+
+    def seconds(self) -> dict:
+        self.marks[-1][1].synchronize()
+        out = {}
+        for (_, a), (name, b) in zip(self.marks, self.marks[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) / 1e3
+        return out
+
+
+def build_sharded(tensor, params: PartitionParams, device="cuda") -> DeviceShardedTensor:
+    """The reference's ``build_sharded(tensor, params)`` (layout.py:462-531):
+    `tensor` is a :class:`~.coo.CooTensor` -- this package's or the
+    reference's, anything with ``dims``, ``subs`` and ``vals`` -- already
+    validated on construction (no duplicates), so the device build skips its
+    own duplicate check."""
+    dims = tuple(int(d) for d in tensor.dims)
+    if tuple(params.dims) != dims:
+        raise ValueError("params were selected for different dims")
+    nnz = int(np.asarray(tensor.vals).shape[0])
+    if params.nnz != nnz:
+        raise ValueError("params were selected for a different nonzero count")
+    return build_device_sharded(tensor.subs, tensor.vals, params, device=device,
+                                check_duplicates=False)
+
+
+def build_device_sharded(subs, vals, params: PartitionParams, device="cuda",
+                         check_duplicates: bool = True) -> DeviceShardedTensor:
     """Device build of the FLYCOO layout (layout.py:462-531 + the B200
     intra-shard order).  `subs` (nnz, N) and `vals` (nnz,) in input order,
-    as numpy arrays or torch tensors (any device)."""
+    as numpy arrays or torch tensors (any device).  Raises ValueError on
+    duplicate coordinates (coo.py:88-89) unless `check_duplicates` is False
+    (inputs that are duplicate-free by construction).  The stage times land
+    in ``st.build_stages`` (seconds, CUDA events)."""
     L = _lib.load()
     dev = torch.device(device)
     subs_t = torch.as_tensor(subs)
@@ -436,8 +584,17 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
         raise ValueError("nnz must fit uint32 positions")
     if max(params.dims) >= 1 << 31:
         raise ValueError("dims must fit int32 coordinates")
+    clock = _StageClock()
     coords = subs_t.to(device=dev, dtype=torch.int32).contiguous()
     fvals = vals_t.to(device=dev, dtype=torch.float32).contiguous()
+    clock.mark("upload")
+    if check_duplicates:
+        if nnz and (int(coords.min()) < 0 or bool((coords.max(0).values.cpu()
+                                                   >= torch.as_tensor(params.dims)).any())):
+            raise ValueError("coordinates outside the declared dims")
+        if device_has_duplicates(coords, params.dims):
+            raise ValueError("duplicate coordinates (coalesce first)")
+        clock.mark("duplicate_check")
     st = _stream_ptr()
     P = lambda t: t.data_ptr() if t is not None else None
     m_arr = _lib.i64_array(params.m)
@@ -481,6 +638,7 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
         morton = sort_by(morton, 1, W - 64)
     del ids, hi, lo
     hi = lo = None
+    clock.mark("morton_order")
 
     counts_all, sids = [], []
     hist = torch.empty(max(params.k), dtype=torch.int64, device=dev)
@@ -501,6 +659,7 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
         sids.append(sid)
         del order
     plan = plan_from_counts(params, counts_all)
+    clock.mark("super_shards")
 
     gpos = []
     for n in range(N):
@@ -529,8 +688,10 @@ def build_device_sharded(subs, vals, params: PartitionParams, device="cuda") -> 
     _lib.call("fc_build_records_scatter", P(gpos[0]), nnz, N, P(coords), P(fvals), P(crd[0]),
               P(val[0]), st)
     del gpos
-    torch.cuda.current_stream().synchronize()
-    return DeviceShardedTensor(plan, crd, val, tuple(slot_maps), dev)
+    clock.mark("shards_slots_records")
+    out = DeviceShardedTensor(plan, crd, val, tuple(slot_maps), dev)
+    out.build_stages = clock.seconds()
+    return out
 
 
 def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
@@ -565,7 +726,9 @@ def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
     P = lambda t: t.data_ptr()
     m_arr = _lib.i64_array(params.m)
     k_arr = _lib.i64_array(params.k)
+    clock = _StageClock()
     crd = records.to(dev).contiguous()
+    clock.mark("upload")
 
     other = torch.empty((nnz, 4), dtype=torch.int32, device=dev)
     A, B, C, D = (other.view(-1)[i * nnz:(i + 1) * nnz] for i in range(4))
@@ -584,6 +747,7 @@ def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
     _lib.call("fc_build_morton32", P(crd), nnz, N, 4, m_arr, k_arr, P(A), st)
     _lib.call("fc_build_iota", P(C), nnz, st)
     sort32(A, C, D, sum(widths))
+    clock.mark("morton_order")
     # canonical orders -> plan and shard ids (S[n])
     counts_all = []
     hist = torch.empty(max(params.k), dtype=torch.int64, device=dev)
@@ -601,6 +765,7 @@ def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
         _lib.call("fc_build_shard_ids", P(C), nnz, P(crd), 4, n, params.m[n], P(offs), P(first),
                   params.g, P(S[n]), st)
     plan = plan_from_counts(params, counts_all)
+    clock.mark("super_shards")
 
     # the input records wait on the host; their device memory holds positions
     # (the caller's tensor is overwritten: it becomes the back buffer)
@@ -628,5 +793,107 @@ def build_device_sharded_lean(records, params: PartitionParams, device="cuda",
         _lib.call("fc_build_scatter_rec16", P(pos[0][a:b]), b - a, P(stage), P(other), st)
         del stage
     del host
-    torch.cuda.current_stream().synchronize()
-    return DeviceShardedTensor(plan, [other, back], [None, None], tuple(S), dev)
+    clock.mark("shards_slots_records")
+    out = DeviceShardedTensor(plan, [other, back], [None, None], tuple(S), dev)
+    out.build_stages = clock.seconds()
+    return out
+
+
+# -------------------------------------------------------------- validation
+
+@dataclass(frozen=True)
+class CheckResult:
+    """One structural check of :func:`validate_plan` (layout.py:537-548)."""
+    name: str
+    passed: bool
+    detail: str = ""
+
+    def line(self) -> str:
+        mark = "pass" if self.passed else "FAIL"
+        suffix = f" ({self.detail})" if self.detail and not self.passed else ""
+        return f"[{mark}] {self.name}{suffix}"
+
+
+@dataclass(frozen=True)
+class PlanReport:
+    checks: tuple
+
+    @property
+    def passed(self) -> bool:
+        return all(c.passed for c in self.checks)
+
+    def first_failure(self):
+        return next((c for c in self.checks if not c.passed), None)
+
+    def format(self) -> str:
+        return "\n".join(c.line() for c in self.checks)
+
+
+def validate_plan(st: DeviceShardedTensor, source=None) -> PlanReport:
+    """The reference's structural gate (layout.py:565-640) over the device
+    tensor's host views: per mode, super-shard conservation, strictly rising
+    shard offsets 0..nnz, every non-final shard holding exactly g elements,
+    shard ids in range and each element inside its super-shard's interval;
+    the active buffer in the active mode's shard order; the double buffer's
+    byte count; and, given the source CooTensor, conservation of the
+    nonzero multiset."""
+    plan, params = st.plan, st.params
+    N, nnz = st.num_modes, st.nnz
+    checks = []
+    sids, idxs, vals = st.active_arrays()
+    for n in range(N):
+        total = int(plan.ss_counts[n].sum())
+        checks.append(CheckResult(f"mode{n}-ss-conservation", total == nnz,
+                                  f"super-shard fills sum to {total}, expected {nnz}"))
+    for n in range(N):
+        offs = plan.shard_offsets[n]
+        ok = bool(np.all(np.diff(offs) > 0)) and int(offs[0]) == 0 and int(offs[-1]) == nnz
+        checks.append(CheckResult(f"mode{n}-offsets", ok,
+                                  "shard offsets must rise strictly from 0 to nnz"))
+        fills = plan.shard_fills(n)
+        last = plan.ss_first_shard[n][1:] - 1
+        interior = np.ones(plan.total_shards(n), dtype=bool)
+        interior[last[plan.ss_shard_counts[n] > 0]] = False
+        bad = np.nonzero(fills[interior] != params.g)[0]
+        checks.append(CheckResult(f"mode{n}-shard-fill", bad.size == 0,
+                                  f"{bad.size} non-final shards not holding exactly g={params.g}"))
+    for n in range(N):
+        nshards = plan.total_shards(n)
+        inrange = (sids[:, n] >= 0) & (sids[:, n] < nshards)
+        if not inrange.all():
+            e = int(np.argmin(inrange))
+            checks.append(CheckResult(f"mode{n}-sid-range", False,
+                                      f"element {e}: shard id {int(sids[e, n])} outside [0, {nshards})"))
+            continue
+        want = idxs[:, n] // params.m[n]
+        got = plan.ss_of_shard(n)[sids[:, n]]
+        ok = bool(np.array_equal(want, got))
+        detail = ""
+        if not ok:
+            e = int(np.argmax(want != got))
+            detail = (f"element {e}: index {int(idxs[e, n])} lies in interval {int(want[e])} but "
+                      f"shard id {int(sids[e, n])} belongs to super-shard {int(got[e])}")
+        checks.append(CheckResult(f"mode{n}-interval-containment", ok, detail))
+    am = st.active_mode
+    expected = np.repeat(np.arange(plan.total_shards(am), dtype=np.int64), plan.shard_fills(am))
+    ok = bool(np.array_equal(sids[:, am], expected))
+    detail = ""
+    if not ok:
+        e = int(np.argmax(sids[:, am] != expected))
+        detail = f"position {e}: shard id {int(sids[e, am])}, plan assigns {int(expected[e])}"
+    checks.append(CheckResult("active-order", ok, detail))
+    acc = st.accounting()
+    # stored bytes per record: the logical int32 coordinates + fp32 value,
+    # padded to 32 B rows for N >= 5 (include/flycoo.h)
+    L = _lib.load()
+    stored = 4 * int(L.fc_crd_words(N)) + (0 if L.fc_value_embedded(N) else 4)
+    want_bytes = 2 * nnz * stored
+    checks.append(CheckResult("double-buffer-bytes", acc["buffer_bytes"] == want_bytes,
+                              f"buffers hold {acc['buffer_bytes']} bytes, expected {want_bytes}"))
+    if source is not None:
+        from .coo import CooTensor
+        ok = CooTensor(tuple(source.dims), np.asarray(source.subs), np.asarray(source.vals)) \
+            .same_nonzeros(CooTensor(tuple(source.dims), idxs, vals))
+        checks.append(CheckResult("conservation", ok,
+                                  "active buffer nonzero multiset differs from the source tensor"))
+    return PlanReport(tuple(checks))

@@ -276,9 +276,20 @@ class PeerShardedTensor:
         """Collective: device pointers of every rank's `tensors` (own ones as
         is, peers' through IPC mappings).  Returns [tensor i][rank q]."""
         bufs = {b.tensor.data_ptr(): b for b in self._bufs}
-        mine = [bufs[t.data_ptr()].handle() for t in tensors]
+        # a local failure still joins the collective (with None), so every
+        # rank raises together instead of leaving the others in the gather
+        try:
+            mine = [bufs[t.data_ptr()].handle() for t in tensors]
+            err = None
+        except Exception as e:  # noqa: BLE001
+            mine, err = None, e
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=self.group)
+        if err is not None:
+            raise err
+        missing = [q for q in range(self.world) if allh[q] is None]
+        if missing:
+            raise RuntimeError(f"ranks {missing} could not export their IPC handles")
         out = [[0] * self.world for _ in tensors]
         for q in range(self.world):
             for i, t in enumerate(tensors):
@@ -364,6 +375,14 @@ class PeerShardedTensor:
         srcv = None if self.val[a] is None else self.val[a].data_ptr() - p.e_lo * 4
         slots = p.global_slots.data_ptr() - p.e_lo * 4 if p.count else None
         pv = None if self.peer_val is None else _lib.ptr_array(self.peer_val[b])
+        if not w.acc_in_smem:
+            # the general kernel accumulates straight into `out` (one chunk
+            # per super-shard, owned by this GPU): the owned rows start at 0
+            # on every pass, also when `out` is reused across sweeps
+            lo, hi = self.owned_rows(mode)
+            if hi > lo:
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=self.device)):
+                    out[lo:hi].zero_()
         _lib.call("fc_mode_worker_peers", src, srcv,
                   _lib.ptr_array([f.data_ptr() for f in factors]), _lib.i64_array(params.dims),
                   out.data_ptr(), self.num_modes, mode, R, params.dims[mode], params.m[mode],

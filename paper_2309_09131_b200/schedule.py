@@ -3,7 +3,7 @@
 The reference assigns super-shards to CPU threads with greedy LPT
 (/root/reference/pkg/src/modecycle/schedule.py:33-86).  On the B200 the work
 decomposition is per-CTA chunks (layout.make_mode_work), so the engine only
-*validates* a ScheduleMap (engine.py:274-277) and ignores its assignment.
+*validates* a ScheduleMap (engine.py:186-189) and ignores its assignment.
 The type and the builder are kept so callers of the reference API run
 unchanged.
 """

@@ -19,6 +19,8 @@ from __future__ import annotations
 import math
 from typing import Sequence
 
+import os
+
 import numpy as np
 import torch
 
@@ -291,6 +293,38 @@ def philox4x32_10(c0, c1, c2, c3, seed: int):
     return c0, c1, c2, c3
 
 
+def _parallel_chunks(n: int, fn, chunk: int = 1 << 22) -> None:
+    """fn(lo, hi) over [0, n) in chunks on the host's cores (numpy releases
+    the GIL inside its ufuncs)."""
+    spans = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]
+    if len(spans) <= 1:
+        for lo, hi in spans:
+            fn(lo, hi)
+        return
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(spans), os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda sp: fn(*sp), spans))
+
+
+def _first_occurrences(rows: np.ndarray, dims) -> np.ndarray:
+    """Index of the first occurrence of every distinct row (any order): a
+    stable sort of the row-major flattened key when prod(dims) fits 63 bits,
+    else a stable lexsort of the columns -- np.unique(rows, axis=0) sorts a
+    void view and took minutes at c2's 96M draws."""
+    from .coo import coords_key
+    key = coords_key(rows, dims)
+    if key is not None:
+        o = np.argsort(key, kind="stable")
+        k = key[o]
+    else:
+        o = np.lexsort(rows.T[::-1])
+        k = rows[o]
+    new = np.ones(len(o), dtype=bool)
+    if len(o) > 1:
+        new[1:] = (k[1:] != k[:-1]) if k.ndim == 1 else np.any(k[1:] != k[:-1], axis=1)
+    return o[new]
+
+
 def zipf_tensor_host(dims: Sequence[int], nnz: int, seed: int, exponents: Sequence,
                      draw_factor: float = 1.25):
     """numpy twin of :func:`zipf_tensor` (identical output; for CPU-side
@@ -298,27 +332,38 @@ def zipf_tensor_host(dims: Sequence[int], nnz: int, seed: int, exponents: Sequen
     dims = tuple(int(d) for d in dims)
     N = len(dims)
     cdfs = [None if s is None else zipf_cdf(d, s) for d, s in zip(dims, exponents)]
-    ndraws = int(nnz * draw_factor) + 1024
-    while True:
-        j = np.arange(ndraws, dtype=np.uint64)
-        rows = np.empty((ndraws, N), dtype=np.int64)
+
+    def draw(rows, lo, hi):
+        j = np.arange(lo, hi, dtype=np.uint64)
         for w in range(N):
             x, y, _, _ = philox4x32_10(j, j >> np.uint64(32), np.uint64(w), np.uint64(0x5EED), seed)
             u = ((x >> np.uint64(5)) * np.uint64(67108864) + (y >> np.uint64(6))).astype(np.float64)
             u *= 1.0 / 9007199254740992.0
             if cdfs[w] is None:
-                rows[:, w] = np.minimum((u * dims[w]).astype(np.int64), dims[w] - 1)
+                rows[lo:hi, w] = np.minimum((u * dims[w]).astype(np.int64), dims[w] - 1)
             else:
-                rows[:, w] = np.searchsorted(cdfs[w], u, side="right")
-        _, first = np.unique(rows, axis=0, return_index=True)
+                rows[lo:hi, w] = np.searchsorted(cdfs[w], u, side="right")
+
+    ndraws = int(nnz * draw_factor) + 1024
+    rows = np.empty((0, N), dtype=np.int64)
+    while True:
+        done = rows.shape[0]  # draws are indexed by j: a retry only adds the new ones
+        rows = np.concatenate([rows, np.empty((ndraws - done, N), dtype=np.int64)])
+        _parallel_chunks(ndraws - done, lambda lo, hi: draw(rows, done + lo, done + hi))
+        first = _first_occurrences(rows, dims)
         if first.size >= nnz:
             subs = rows[np.sort(first)[:nnz]]
             break
         ratio = nnz / max(first.size, 1)
         ndraws = int(ndraws * max(1.2, min(4.0, ratio * 1.1))) + 1024
-    i = np.arange(nnz, dtype=np.uint64)
-    x, _, _, _ = philox4x32_10(i, i >> np.uint64(32), np.uint64(77), np.uint64(0xF00D), seed)
-    vals = (((x >> np.uint64(8)).astype(np.float64) + 1.0) * (1.0 / 16777216.0)).astype(np.float32)
+    vals = np.empty(nnz, dtype=np.float32)
+
+    def draw_vals(lo, hi):
+        i = np.arange(lo, hi, dtype=np.uint64)
+        x, _, _, _ = philox4x32_10(i, i >> np.uint64(32), np.uint64(77), np.uint64(0xF00D), seed)
+        vals[lo:hi] = ((x >> np.uint64(8)).astype(np.float64) + 1.0) * (1.0 / 16777216.0)
+
+    _parallel_chunks(nnz, draw_vals)
     return subs, vals
 
 

@@ -240,6 +240,57 @@ def golden_io():
                         dims=np.asarray(t2.dims), synth_subs=t.subs, synth_vals=t.vals)
 
 
+def golden_boundary():
+    """The reference-facing call shapes: FactorSet.random
+    streams (coo.py:184-192); CooTensor validation errors (coo.py:65-89);
+    validate_plan's check list on a fresh build (layout.py:565-640); and the
+    reference's own call sequence select_params -> build_sharded(tensor,
+    params) -> schedule_super_shards -> sweep_all_modes(st,
+    FactorSet.random(dims, R, seed), smap) (bench.py:119-134)."""
+    out = {}
+    for i, (dims, rank, seed) in enumerate([((5, 7, 3), 4, 2), ((40, 30, 20, 10), 8, 11),
+                                            ((1000, 800, 600), 16, 1001)]):
+        fs = mc.FactorSet.random(dims, rank, seed)
+        out[f"rand{i}_dims"] = np.asarray(dims)
+        out[f"rand{i}_rank"] = np.asarray(rank)
+        out[f"rand{i}_seed"] = np.asarray(seed)
+        for n, f in enumerate(fs.factors):
+            out[f"rand{i}_f{n}"] = f
+    errors = {}
+    for name, (dims, subs, vals) in {
+        "one_mode": ((5,), [[1]], [1.0]),
+        "zero_dim": ((5, 0), [[1, 0]], [1.0]),
+        "empty": ((5, 4), np.zeros((0, 2), np.int64), np.zeros(0)),
+        "misaligned": ((5, 4), [[1, 1], [2, 2]], [1.0]),
+        "nonfinite": ((5, 4), [[1, 1]], [np.inf]),
+        "negative": ((5, 4), [[-1, 1]], [1.0]),
+        "out_of_range": ((5, 4), [[5, 1]], [1.0]),
+        "duplicate": ((5, 4), [[1, 1], [2, 2], [1, 1]], [1.0, 2.0, 3.0]),
+    }.items():
+        try:
+            mc.CooTensor(dims, subs, vals)
+            errors[name] = ""
+        except ValueError as e:
+            errors[name] = str(e)
+    out["coo_errors"] = np.asarray(json.dumps(errors))
+    t = mc.synth_tensor((60, 50, 40), 20_000, seed=9, skew=0.5)
+    params = mc.select_params(t.dims, t.nnz, 4, 1 << 16, 16, g_range=(64, 1024))
+    st = mc.build_sharded(t, params)
+    smap = mc.schedule_super_shards(st.plan, 4)
+    report = mc.validate_plan(st, t)
+    out["validate_names"] = np.asarray(json.dumps([c.name for c in report.checks]))
+    out["validate_passed"] = np.asarray([c.passed for c in report.checks])
+    fs = mc.FactorSet.random(t.dims, 16, 77)
+    res = mc.sweep_all_modes(st, fs, smap, remap="slot")
+    out["seq_subs"] = t.subs
+    out["seq_vals"] = t.vals
+    out["seq_m"] = np.asarray(params.m)
+    out["seq_g"] = np.asarray(params.g)
+    for n, f in enumerate(res.factors):
+        out[f"seq_out{n}"] = f
+    np.savez_compressed(OUT / "boundary.npz", **out)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nc")
     only = os.environ.get("GOLDEN_ONLY")  # e.g. GOLDEN_ONLY=cpals regenerates one fixture
@@ -253,4 +304,5 @@ if __name__ == "__main__":
     golden_schedule()
     golden_cpals()
     golden_io()
+    golden_boundary()
     print("golden fixtures written to", OUT)

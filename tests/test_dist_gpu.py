@@ -63,7 +63,7 @@ def _worker(rank, world, port, result):
             st = build_device_sharded(coords, vals, params)
             ref_st = build_device_sharded(coords, vals, params)
             dt = DistShardedTensor(st, world, rank)
-            f0 = DeviceFactorSet.random(dims, 32, seed=3)
+            f0 = DeviceFactorSet.random_device(dims, 32, seed=3)
             ops = StagedOps()
             working = list(f0.factors)
             ref_working = list(f0.factors)

@@ -105,7 +105,7 @@ def _run(cfg: int, full_oracle: bool):
         del coords, vals
     torch.cuda.empty_cache()
     smap = schedule_super_shards(st.plan, 1)
-    fs = DeviceFactorSet.random(dims, R, seed=2000 + cfg)
+    fs = DeviceFactorSet.random_device(dims, R, seed=2000 + cfg)
     f64 = [f.double().cpu().numpy() for f in fs.factors]
     start = _checksum(st.crd[st.active])
     rng = np.random.default_rng(cfg)

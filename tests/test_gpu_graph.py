@@ -24,13 +24,13 @@ def test_graph_replay_matches_eager(N):
     from paper_2309_09131_b200 import DeviceFactorSet, sweep_all_modes
     from paper_2309_09131_b200.graph import SweepGraph
     dims, st, ref, smap = _case(N)
-    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    f0 = DeviceFactorSet.random_device(dims, 32, seed=5)
     g = SweepGraph(st, f0, smap)
     # the constructor's warm-up sweeps moved st; bring ref to the same parity
     for _ in range(1 if N % 2 == 0 else 2):
         sweep_all_modes(ref, f0, smap)
     for rep in range(4):
-        fs = DeviceFactorSet.random(dims, 32, seed=10 + rep)
+        fs = DeviceFactorSet.random_device(dims, 32, seed=10 + rep)
         got = g.run(fs)
         want = sweep_all_modes(ref, fs, smap)
         assert st.active == ref.active and st.active_mode == ref.active_mode == 0
@@ -43,7 +43,7 @@ def test_graph_replay_chained_inputs_and_errors():
     from paper_2309_09131_b200 import DeviceFactorSet, ShardOverflowError, sweep_all_modes
     from paper_2309_09131_b200.graph import SweepGraph
     dims, st, ref, smap = _case(3, 100_000)
-    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    f0 = DeviceFactorSet.random_device(dims, 32, seed=5)
     g = SweepGraph(st, f0, smap)
     for _ in range(2):
         sweep_all_modes(ref, f0, smap)
@@ -65,7 +65,7 @@ def test_graph_host_io_matches_eager():
     from paper_2309_09131_b200 import DeviceFactorSet, sweep_all_modes
     from paper_2309_09131_b200.graph import SweepGraph
     dims, st, ref, smap = _case(3, 100_000)
-    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    f0 = DeviceFactorSet.random_device(dims, 32, seed=5)
     g = SweepGraph(st, f0, smap)
     for _ in range(2):
         sweep_all_modes(ref, f0, smap)
@@ -73,7 +73,7 @@ def test_graph_host_io_matches_eager():
     host_out = [torch.empty(f.shape, dtype=torch.float32).pin_memory() for f in f0.factors]
     g.bind_host(host_in, host_out)
     for rep in range(3):
-        fs = DeviceFactorSet.random(dims, 32, seed=20 + rep)
+        fs = DeviceFactorSet.random_device(dims, 32, seed=20 + rep)
         for h, f in zip(host_in, fs.factors):
             h.copy_(f.cpu())
         outs = g.run_host()
@@ -89,11 +89,11 @@ def test_graph_fixed_factor_loop_matches_eager():
     from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, sweep_all_modes
     from paper_2309_09131_b200.graph import SweepGraph
     dims, st, ref, smap = _case(4, 100_000)
-    f0 = DeviceFactorSet.random(dims, 32, seed=5)
+    f0 = DeviceFactorSet.random_device(dims, 32, seed=5)
     g = SweepGraph(st, f0, smap, updated=False)
     sweep_all_modes(ref, f0, smap)  # N = 4: one warm-up sweep
     for rep in range(3):
-        fs = DeviceFactorSet.random(dims, 32, seed=30 + rep)
+        fs = DeviceFactorSet.random_device(dims, 32, seed=30 + rep)
         got = g.run(fs)
         want = [mttkrp_mode(ref, fs, n, smap) for n in range(4)]
         for a, b in zip(got.factors, want):

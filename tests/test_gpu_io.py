@@ -17,7 +17,7 @@ def test_flycoo_image_roundtrip(tmp_path, dims):
     coords, vals = zipf_tensor(dims, 300_000, seed=4, exponents=(1.1,) * len(dims))
     params = device_params(dims, 300_000, 32, g=4096)
     st = build_device_sharded(coords, vals, params)
-    fs = DeviceFactorSet.random(dims, 32, seed=1)
+    fs = DeviceFactorSet.random_device(dims, 32, seed=1)
     smap = schedule_super_shards(st.plan, 1)
     mttkrp_mode(st, fs, 0, smap)  # save a non-zero active mode
     path = tmp_path / "t.flycoo"
@@ -36,7 +36,7 @@ def test_flycoo_image_roundtrip(tmp_path, dims):
 
 
 def test_mcfd_roundtrip_device(tmp_path):
-    fs = DeviceFactorSet.random((50, 70, 30), 8, seed=3)
+    fs = DeviceFactorSet.random_device((50, 70, 30), 8, seed=3)
     fs.lambdas[:] = [1, 2, 3, 4, 5, 6, 7, 8]
     p = tmp_path / "f.mcfd"
     fio.save_factor_set(fs, p)

@@ -64,7 +64,7 @@ def test_lean_sweep_bitwise():
     from paper_2309_09131_b200 import DeviceFactorSet, schedule_super_shards, sweep_all_modes
     dims, m = (46, 3000, 3000), (46, 64, 64)
     ref, lean = _both_builds(dims, (None, 1.0, 1.0), 400_000, m, 2048)
-    fs = DeviceFactorSet.random(dims, 16, seed=3)
+    fs = DeviceFactorSet.random_device(dims, 16, seed=3)
     a = sweep_all_modes(ref, fs, schedule_super_shards(ref.plan, 1))
     b = sweep_all_modes(lean, fs, schedule_super_shards(lean.plan, 1))
     for x, y in zip(a.factors, b.factors):

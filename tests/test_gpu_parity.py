@@ -371,7 +371,7 @@ def test_packed_and_unpacked_modes_in_one_sweep():
 
 
 def test_remap_store_single_element_mirror():
-    """remap_store / RemapCursors (engine.py:182-223): first store lands at the
+    """remap_store / RemapCursors (engine.py:94-135): first store lands at the
     shard base, a full shard raises ShardOverflowError."""
     from paper_2309_09131_b200 import RemapCursors, remap_store
     z, N, params = _golden("n3_small")

@@ -21,27 +21,28 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _case(N, nnz=400_000):
+def _case(N, nnz=400_000, m=16):
     from paper_2309_09131_b200 import build_device_sharded, device_params
     from paper_2309_09131_b200.synth import zipf_tensor
     dims = {3: (3000, 2000, 2500), 4: (300, 400, 250, 90), 5: (60, 50, 40, 30, 20)}[N]
     coords, vals = zipf_tensor(dims, nnz, seed=6, exponents=(1.1,) * N)
-    params = device_params(dims, nnz, 32, g=4096, m=[16] * N)
+    params = device_params(dims, nnz, 32, g=4096, m=[m] * N)
     return dims, coords, vals, params, build_device_sharded
 
 
-def _virtual_sweep(N, world, sweeps=2):
+def _virtual_sweep(N, world, sweeps=2, m=16):
     from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, schedule_super_shards
     from paper_2309_09131_b200.peer import PeerShardedTensor
-    dims, coords, vals, params, build = _case(N)
+    dims, coords, vals, params, build = _case(N, m=m)
     st = build(coords, vals, params)
     ref = build(coords, vals, params)
     ranks = [PeerShardedTensor(st, world, r, ipc=False) for r in range(world)]
     PeerShardedTensor.connect_local(ranks)
     # the Zipf head super-shard is split: some GPU runs chunks another owns
-    assert any(bool((dt.plans[n].chunk_owner != dt.rank).any())
+    # (shared-memory accumulator tiles; global accumulation never splits)
+    assert not ranks[0].works[0].acc_in_smem or any(bool((dt.plans[n].chunk_owner != dt.rank).any())
                for dt in ranks for n in range(N)), "no split super-shard in this case"
-    f0 = DeviceFactorSet.random(dims, 32, seed=3)
+    f0 = DeviceFactorSet.random_device(dims, 32, seed=3)
     working = [list(f0.factors) for _ in range(world)]
     ref_working = list(f0.factors)
     smap = schedule_super_shards(ref.plan, 1)
@@ -74,6 +75,37 @@ def _virtual_sweep(N, world, sweeps=2):
         dt.check()
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_store_virtual_ranks_global_accumulator(world):
+    """m = 600 rows at R = 32 (75 KB tiles): the general kernel accumulates
+    in `out`, which PeerShardedTensor reuses across sweeps -- the owned rows
+    must be re-zeroed every pass (second sweep bit-exact)."""
+    torch.cuda.set_device(0)
+    _virtual_sweep(3, world, sweeps=2, m=600)
+
+
+def test_stream_wait_flush_query_and_graph_capture():
+    """The flush capability is a per-device attribute query (no failing
+    wait probes); a signal + wait pair on the same stream captures into a
+    CUDA graph and replays."""
+    from paper_2309_09131_b200 import _lib
+    torch.cuda.set_device(0)
+    L = _lib.load()
+    assert L.fc_stream_wait_flush_supported() in (0, 1)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            _lib.call("fc_stream_signal", flag.data_ptr(), 1, s.cuda_stream)
+            _lib.call("fc_stream_wait", flag.data_ptr(), 1, s.cuda_stream)
+            _lib.call("fc_stream_signal", flag.data_ptr(), 0, s.cuda_stream)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+
+
 @pytest.mark.parametrize("N", [3, 4, 5])
 @pytest.mark.parametrize("world", [2, 3])
 def test_peer_store_virtual_ranks(N, world):
@@ -90,7 +122,7 @@ def test_peer_store_slot_out_of_range_flags():
     ranks = [PeerShardedTensor(st, 2, r, ipc=False) for r in range(2)]
     PeerShardedTensor.connect_local(ranks)
     ranks[0].plans[0].global_slots[5] = -2  # 0xFFFFFFFE
-    f = list(DeviceFactorSet.random(dims, 32, seed=1).factors)
+    f = list(DeviceFactorSet.random_device(dims, 32, seed=1).factors)
     out = ranks[0].output(0, 32)[0]
     ranks[0].mode_pass(f, 0, out)
     with pytest.raises(RuntimeError, match="flags 0x1"):
@@ -119,7 +151,7 @@ def _ipc_worker(rank, world, port, result, sync):
             dt = PeerShardedTensor(st, world, rank)
             dt.connect()
             assert dt.device_sync == (sync == "device")
-            f0 = DeviceFactorSet.random(dims, 32, seed=3)
+            f0 = DeviceFactorSet.random_device(dims, 32, seed=3)
             ref_working = list(f0.factors)
             got = list(f0.factors)
             smap = schedule_super_shards(ref.plan, 1)

@@ -44,7 +44,7 @@ def main():
     st = build_device_sharded(coords, vals, params, device=dev)
     del coords, vals
     smap = schedule_super_shards(st.plan, 1)
-    fs = DeviceFactorSet.random(dims, R, seed=1, device=dev)
+    fs = DeviceFactorSet.random_device(dims, R, seed=1, device=dev)
     N = len(dims)
     L = _lib.load()
     L.fc_exp_set_chunk_order.argtypes = [ctypes.c_void_p]

@@ -15,7 +15,7 @@ coords, vals = config_tensor(2, device=dev)
 dims = (12092, 9184, 28818)
 params = device_params(dims, coords.shape[0], 32)
 st = build_device_sharded(coords, vals, params, device=dev)
-fs = DeviceFactorSet.random(dims, 32, seed=1, device=dev)
+fs = DeviceFactorSet.random_device(dims, 32, seed=1, device=dev)
 crd = st.crd[0]
 idx = torch.stack([crd[:, 1], crd[:, 2]], dim=1).contiguous()
 n = idx.shape[0]

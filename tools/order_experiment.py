@@ -17,7 +17,7 @@ dims, R, N = (12092, 9184, 28818), 32, 3
 params = device_params(dims, coords.shape[0], R)
 st = build_device_sharded(coords, vals, params, device=dev)
 nnz = st.nnz
-fs = DeviceFactorSet.random(dims, R, seed=1002, device=dev)
+fs = DeviceFactorSet.random_device(dims, R, seed=1002, device=dev)
 fptrs = _lib.ptr_array([f.data_ptr() for f in fs.factors])
 strm = torch.cuda.current_stream().cuda_stream
 

@@ -15,7 +15,7 @@ coords, vals = config_tensor(2, device=dev)
 dims, R = (12092, 9184, 28818), 32
 params = device_params(dims, coords.shape[0], R)
 st = build_device_sharded(coords, vals, params, device=dev)
-fs = DeviceFactorSet.random(dims, R, seed=1002, device=dev)
+fs = DeviceFactorSet.random_device(dims, R, seed=1002, device=dev)
 fptrs = _lib.ptr_array([f.data_ptr() for f in fs.factors])
 strm = torch.cuda.current_stream().cuda_stream
 

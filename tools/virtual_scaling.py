@@ -49,7 +49,7 @@ def main():
     st = build_device_sharded(coords, vals, params, device=dev)
     del coords, vals
     N = len(dims)
-    fs = DeviceFactorSet.random(dims, R, seed=1, device=dev)
+    fs = DeviceFactorSet.random_device(dims, R, seed=1, device=dev)
     result = {"config": cfg, "nnz": int(st.nnz), "modes": {}}
     base = None
     for P in (1, 2, 4, 8):
