@@ -38,7 +38,7 @@ extern "C" {
 /* Bits of the device flag word (int32) written by fc_mode_worker /
  * fc_remap_cursor.  The host shim raises ShardOverflowError for
  * FC_FLAG_SLOT_RANGE / FC_FLAG_SHARD_OVERFLOW and BufferOrderError for
- * FC_FLAG_ROW_OUTSIDE_SS (engine.py:129-134, 343-351). */
+ * FC_FLAG_ROW_OUTSIDE_SS (engine.py:41-46, 255-263). */
 #define FC_FLAG_SLOT_RANGE 1      /* a destination slot >= nnz              */
 #define FC_FLAG_ROW_OUTSIDE_SS 2  /* element's output row not in its chunk's
                                      super-shard: buffer not ordered for mode */
