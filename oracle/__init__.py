@@ -17,6 +17,9 @@ the C kernel in ``flycoo_oracle.c``:
   reference, elements inside a shard ordered by (previous-mode shard id,
   Morton hi, lo, input position).  Restated here so the GPU build is checked
   bit-exactly.
+* :func:`shard_hashes`        -- layout.py:474-497 streamed (C): per-shard
+  (hash, count) digests of the canonical shard assignment for tensors whose
+  full canonical_build does not fit the host (c3-c5), with :func:`elem_hash`
 * :func:`lpt_schedule`        -- schedule.py:57-66 (greedy LPT)
 * :class:`OracleTensor`       -- engine.py:163-293 (mttkrp_mode /
   sweep_all_modes over the reference's int64/float64 double buffer, workers
@@ -76,6 +79,11 @@ def lib():
                 ctypes.c_int, _i64p]
             L.orc_stable_sort_u64.restype = ctypes.c_int
             L.orc_stable_sort_u64.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int, _i64p]
+            L.orc_shard_hashes.restype = ctypes.c_int
+            L.orc_shard_hashes.argtypes = [
+                ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                ctypes.c_int, ctypes.c_int, _i64p, _i64p, ctypes.c_int64, ctypes.c_int, _i64p,
+                _u64p, _i64p]
             L.orc_reference_mttkrp.restype = None
             L.orc_reference_mttkrp.argtypes = [
                 _i64p, _f64p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_f64p),
@@ -244,6 +252,77 @@ def shard_multiset_keys(coords: np.ndarray, vals_bits: np.ndarray, shard_offsets
     keys = [vals_bits] + [coords[:, w] for w in range(N - 1, -1, -1)] + [sid]
     o = np.lexsort(keys)
     return coords[o], vals_bits[o]
+
+
+# ------------------------------------------------------------- shard digests
+
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    x = x ^ (x >> np.uint64(30))
+    x = x * _M1
+    x = x ^ (x >> np.uint64(27))
+    x = x * _M2
+    return x ^ (x >> np.uint64(31))
+
+
+def elem_hash(coords: np.ndarray, vbits: np.ndarray) -> np.ndarray:
+    """Per-element digest of (int32 coordinates, fp32 value bits), the same
+    function as orc_elem_hash (flycoo_oracle.c)."""
+    coords = np.asarray(coords)
+    h = np.full(coords.shape[0], 0x9E3779B97F4A7C15, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for w in range(coords.shape[1]):
+            h = _mix64(h ^ coords[:, w].astype(np.uint32).astype(np.uint64))
+        v = np.asarray(vbits).astype(np.uint32).astype(np.uint64)
+        return _mix64(h ^ ((v << np.uint64(32)) | np.uint64(0x5BD1E995)))
+
+
+def shard_digests_from_ids(coords, vbits, shard_ids, nshards: int):
+    """(hash, count) per shard from explicit shard ids (wrapping sums)."""
+    h = elem_hash(coords, vbits)
+    out = np.zeros(nshards, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        np.add.at(out, np.asarray(shard_ids, dtype=np.int64), h)
+    cnt = np.bincount(np.asarray(shard_ids, dtype=np.int64), minlength=nshards).astype(np.int64)
+    return out, cnt
+
+
+def shard_hashes(records: np.ndarray, nmodes: int, mode: int, m, k, g: int,
+                 vbits: np.ndarray | None = None, threads: int | None = None):
+    """Streaming restatement of the reference's canonical shard assignment
+    (layout.py:474-497) for `mode`, reduced to per-shard (hash, count)
+    digests -- for tensors whose canonical_build does not fit the host
+    (c3-c5).  `records` is (nnz, cs) int32 in input order: coordinates in
+    columns 0..N-1, and the fp32 value bits in column `cs-1` unless `vbits`
+    is given.  Returns (ss_counts, hash uint64 per shard, count per shard)."""
+    records = np.ascontiguousarray(records, dtype=np.int32)
+    nnz, cs = records.shape
+    if vbits is None:
+        vptr, vs = records[:, cs - 1:].ctypes.data, cs
+        keep = records
+    else:
+        keep = np.ascontiguousarray(vbits).view(np.uint32)
+        vptr, vs = keep.ctypes.data, 1
+    m = np.ascontiguousarray(np.asarray(m, dtype=np.int64))
+    k = np.ascontiguousarray(np.asarray(k, dtype=np.int64))
+    K = int(k[mode])
+    ss_counts = np.zeros(K, dtype=np.int64)
+    # shard count is only known after the counts: size for the worst case
+    nsh_max = K + nnz // int(g) + 1
+    hsh = np.zeros(nsh_max, dtype=np.uint64)
+    cnt = np.zeros(nsh_max, dtype=np.int64)
+    rc = lib().orc_shard_hashes(records.ctypes.data, cs, vptr, vs, nnz, int(nmodes), int(mode),
+                                _p(m, _i64p), _p(k, _i64p), int(g),
+                                int(threads or os.cpu_count() or 1), _p(ss_counts, _i64p),
+                                _p(hsh, _u64p), _p(cnt, _i64p))
+    del keep
+    if rc != 0:
+        raise RuntimeError(f"orc_shard_hashes failed ({rc})")
+    nsh = int((-(-ss_counts // int(g))).sum())
+    return ss_counts, hsh[:nsh], cnt[:nsh]
 
 
 # ------------------------------------------------------------------ schedule

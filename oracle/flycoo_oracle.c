@@ -254,3 +254,193 @@ int orc_stable_sort_u64(const uint64_t *keys, int64_t n, int bits, int64_t *orde
   free(cnt); free(tmp); free(kc); free(kt);
   return 0;
 }
+
+/* --------------------------------------------------- streaming shard hashes */
+
+/* Per-shard order-independent digests of the reference's canonical layout
+ * for tensors too large for canonical_build (c3-c5).  For mode
+ * n: super-shard s = c_n / m_n (layout.py:474-476); inside s the canonical
+ * order is (Morton(hi, lo) of every mode's interval coordinate, input
+ * position) (layout.py:477-484, morton.py:20-44); element r of s belongs to
+ * shard first[s] + r / g (layout.py:491-492).  Every element contributes
+ * orc_elem_hash(coords, value bits) to its shard's wrapping 64-bit sum and 1
+ * to its count -- a multiset digest the GPU side recomputes from its buffer.
+ *
+ * coords: int32 rows of stride cs (>= N; the 16-B device records work
+ * directly), vbits: uint32 values of stride vs.  Memory: nnz uint32 ids +
+ * per-thread (key, id) radix scratch of the largest super-shard.  Morton
+ * keys must fit 64 bits (every BASELINE config does).  Returns 0, -1 when out
+ * of memory, -2 when the key needs more than 64 bits. */
+
+static inline uint64_t orc_mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+uint64_t orc_elem_hash(const int32_t *c, int nmodes, uint32_t vbits) {
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  for (int w = 0; w < nmodes; ++w) h = orc_mix64(h ^ (uint64_t)(uint32_t)c[w]);
+  return orc_mix64(h ^ ((uint64_t)vbits << 32 | 0x5bd1e995u));
+}
+
+typedef struct {
+  const int32_t *coords; int64_t cs;
+  const uint32_t *vbits; int64_t vs;
+  int nmodes, mode;
+  const int64_t *m;
+  int widths[16], maxw, total;
+  const uint32_t *ids; const int64_t *ss_off; const int64_t *first; int64_t g;
+  int64_t nss;
+  _Atomic int64_t *next;            /* work queue over super-shards (largest first) */
+  const int64_t *queue;
+  uint64_t *hash; int64_t *count;   /* per shard */
+  int err;
+} orc_hash_job_t;
+
+static uint64_t orc_morton_row(const orc_hash_job_t *J, const int32_t *c) {
+  uint64_t l = 0;
+  int pos = 0;
+  for (int b = 0; b < J->maxw; ++b)
+    for (int w = 0; w < J->nmodes; ++w) {
+      if (b >= J->widths[w]) continue;
+      l |= ((uint64_t)(c[w] / J->m[w]) >> b & 1u) << pos;
+      ++pos;
+    }
+  return l;
+}
+
+static void *orc_hash_run(void *arg) {
+  orc_hash_job_t *J = (orc_hash_job_t *)arg;
+  /* scratch grows to the largest super-shard this thread draws: the queue is
+   * largest-first, so the threads together hold about the sizes of the
+   * `threads` largest super-shards */
+  uint64_t *k0 = NULL, *k1 = NULL;
+  uint32_t *i0 = NULL, *i1 = NULL;
+  int64_t cap = 0;
+  int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * 2049);
+  if (!cnt) { J->err = -1; return NULL; }
+  for (;;) {
+    const int64_t q = atomic_fetch_add(J->next, 1);
+    if (q >= J->nss) break;
+    const int64_t s = J->queue[q];
+    const int64_t lo = J->ss_off[s], n = J->ss_off[s + 1] - lo;
+    if (n == 0) continue;
+    if (n > cap) {
+      free(k0); free(k1); free(i0); free(i1);
+      k0 = (uint64_t *)malloc((size_t)n * 8); k1 = (uint64_t *)malloc((size_t)n * 8);
+      i0 = (uint32_t *)malloc((size_t)n * 4); i1 = (uint32_t *)malloc((size_t)n * 4);
+      cap = n;
+      if (!k0 || !k1 || !i0 || !i1) { J->err = -1; break; }
+    }
+    for (int64_t r = 0; r < n; ++r) {
+      const uint32_t id = J->ids[lo + r];
+      i0[r] = id;
+      k0[r] = orc_morton_row(J, J->coords + (int64_t)id * J->cs);
+    }
+    /* stable LSD radix on the Morton key; ids enter in input order */
+    uint64_t *ka = k0, *kb = k1;
+    uint32_t *ia = i0, *ib = i1;
+    for (int sh = 0; sh < J->total; sh += 11) {
+      memset(cnt, 0, sizeof(int64_t) * 2049);
+      for (int64_t r = 0; r < n; ++r) cnt[((ka[r] >> sh) & 2047) + 1]++;
+      for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
+      for (int64_t r = 0; r < n; ++r) {
+        const int64_t t = cnt[(ka[r] >> sh) & 2047]++;
+        kb[t] = ka[r];
+        ib[t] = ia[r];
+      }
+      uint64_t *tk = ka; ka = kb; kb = tk;
+      uint32_t *ti = ia; ia = ib; ib = ti;
+    }
+    for (int64_t r = 0; r < n; ++r) {
+      const int64_t id = ia[r];
+      const int64_t sh = J->first[s] + r / J->g;
+      J->hash[sh] += orc_elem_hash(J->coords + id * J->cs, J->nmodes, J->vbits[id * J->vs]);
+      J->count[sh] += 1;
+    }
+  }
+  free(k0); free(k1); free(i0); free(i1); free(cnt);
+  return NULL;
+}
+
+/* (count, id) pairs: count descending, id ascending */
+static int orc_cmp_desc(const void *a, const void *b) {
+  const int64_t *x = (const int64_t *)a, *y = (const int64_t *)b;
+  if (x[0] != y[0]) return x[0] > y[0] ? -1 : 1;
+  return (x[1] > y[1]) - (x[1] < y[1]);
+}
+
+int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, int64_t vs,
+                     int64_t nnz, int nmodes, int mode, const int64_t *m, const int64_t *k,
+                     int64_t g, int threads, int64_t *ss_counts, uint64_t *hash,
+                     int64_t *count) {
+  if (nmodes > 16 || threads < 1) return -3;
+  orc_hash_job_t J;
+  memset(&J, 0, sizeof(J));
+  J.coords = coords; J.cs = cs; J.vbits = vbits; J.vs = vs;
+  J.nmodes = nmodes; J.mode = mode; J.m = m; J.g = g;
+  for (int w = 0; w < nmodes; ++w) {
+    J.widths[w] = k[w] > 1 ? bit_length_u64((uint64_t)(k[w] - 1)) : 0;
+    J.total += J.widths[w];
+    if (J.widths[w] > J.maxw) J.maxw = J.widths[w];
+  }
+  if (J.total > 64) return -2;
+  const int64_t K = k[mode];
+  /* super-shard of every element, counts (layout.py:487) */
+  memset(ss_counts, 0, sizeof(int64_t) * K);
+  for (int64_t i = 0; i < nnz; ++i) ss_counts[coords[i * cs + mode] / m[mode]]++;
+  int64_t *off = (int64_t *)malloc(sizeof(int64_t) * (K + 1));
+  int64_t *first = (int64_t *)malloc(sizeof(int64_t) * (K + 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * K);
+  int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * K);
+  uint32_t *ids = (uint32_t *)malloc((size_t)nnz * 4);
+  if (!off || !first || !fill || !queue || !ids) {
+    free(off); free(first); free(fill); free(queue); free(ids);
+    return -1;
+  }
+  off[0] = first[0] = 0;
+  int64_t big = 0;
+  for (int64_t s = 0; s < K; ++s) {
+    off[s + 1] = off[s] + ss_counts[s];
+    first[s + 1] = first[s] + (ss_counts[s] + g - 1) / g;
+    fill[s] = off[s];
+    queue[s] = s;
+    if (ss_counts[s] > big) big = ss_counts[s];
+  }
+  /* stable counting sort of element ids by super-shard (ids ascending) */
+  for (int64_t i = 0; i < nnz; ++i) ids[fill[coords[i * cs + mode] / m[mode]]++] = (uint32_t)i;
+  {
+    int64_t *pairs = (int64_t *)malloc(sizeof(int64_t) * 2 * (K > 0 ? K : 1));
+    if (!pairs) {
+      free(off); free(first); free(fill); free(queue); free(ids);
+      return -1;
+    }
+    for (int64_t s = 0; s < K; ++s) { pairs[2 * s] = ss_counts[s]; pairs[2 * s + 1] = s; }
+    qsort(pairs, (size_t)K, 2 * sizeof(int64_t), orc_cmp_desc);
+    for (int64_t s = 0; s < K; ++s) queue[s] = pairs[2 * s + 1];
+    free(pairs);
+  }
+  memset(hash, 0, sizeof(uint64_t) * first[K]);
+  memset(count, 0, sizeof(int64_t) * first[K]);
+  _Atomic int64_t next = 0;
+  J.ids = ids; J.ss_off = off; J.first = first; J.nss = K; J.next = &next; J.queue = queue;
+  J.hash = hash; J.count = count;
+  /* the largest super-shards go first: one thread holds the largest scratch,
+   * the others the size of the (threads)-th largest */
+  if (threads > K) threads = (int)(K > 0 ? K : 1);
+  (void)big;
+  pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * threads);
+  orc_hash_job_t *jobs = (orc_hash_job_t *)malloc(sizeof(orc_hash_job_t) * threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = J;
+    pthread_create(&tid[t], NULL, orc_hash_run, &jobs[t]);
+  }
+  int err = 0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(tid[t], NULL);
+    if (jobs[t].err) err = jobs[t].err;
+  }
+  free(tid); free(jobs); free(off); free(first); free(fill); free(queue); free(ids);
+  return err;
+}

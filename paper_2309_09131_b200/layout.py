@@ -836,7 +836,7 @@ def validate_plan(st: DeviceShardedTensor, source=None) -> PlanReport:
     shard ids in range and each element inside its super-shard's interval;
     the active buffer in the active mode's shard order; the double buffer's
     byte count; and, given the source CooTensor, conservation of the
-    nonzero multiset."""
+    nonzero multiset (values compared at the device's fp32 precision)."""
     plan, params = st.plan, st.params
     N, nnz = st.num_modes, st.nnz
     checks = []
@@ -891,8 +891,10 @@ def validate_plan(st: DeviceShardedTensor, source=None) -> PlanReport:
     checks.append(CheckResult("double-buffer-bytes", acc["buffer_bytes"] == want_bytes,
                               f"buffers hold {acc['buffer_bytes']} bytes, expected {want_bytes}"))
     if source is not None:
+        # the device holds fp32 values: the source's values rounded to fp32
         from .coo import CooTensor
-        ok = CooTensor(tuple(source.dims), np.asarray(source.subs), np.asarray(source.vals)) \
+        sv = np.asarray(source.vals, dtype=np.float64).astype(np.float32).astype(np.float64)
+        ok = CooTensor(tuple(source.dims), np.asarray(source.subs), sv) \
             .same_nonzeros(CooTensor(tuple(source.dims), idxs, vals))
         checks.append(CheckResult("conservation", ok,
                                   "active buffer nonzero multiset differs from the source tensor"))

@@ -8,17 +8,27 @@ not fit"), through the public API on one B200:
   build): a sample of output rows per mode --
   uniform rows plus moderately heavy ones that span several chunks (K2) --
   recomputed in float64 on the host from the nonzeros that carry them;
-* all three: after every pass every element sits in the super-shard of its
+* all: after every pass every element sits in the super-shard of its
   active mode (BufferOrderError territory, layout.py:474-497), and after N
   remaps the buffer equals the initial one bit-exactly (position-dependent
-  checksum), the size-independent cycle identity.
+  checksum), the size-independent cycle identity;
+* the layout itself after the build and after every remap, against the
+  reference's canonical shard assignment (north_star: "per-shard nonzero
+  multisets and offsets"): c2 exactly -- every nonzero's shard and value
+  against ``oracle.canonical_build`` at the bench's own parameters, plus the
+  shard offsets; c3 and c4 (and c5 with FLYCOO_C5_DIGESTS=1: ~160 GB of host
+  memory) through per-shard (hash, count) digests against the streaming C
+  restatement ``oracle.shard_hashes`` and the shard offsets against the
+  super-shard fills it counts.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
 import oracle
-from gpu_helpers import assert_rel
+from gpu_helpers import assert_rel, device_shard_digests
 
 pytestmark = pytest.mark.gpu
 
@@ -81,7 +91,80 @@ def _sample_rows(st, mode: int, rows: np.ndarray, factors64):
     return out.numpy()[rows], len(vals)
 
 
-def _run(cfg: int, full_oracle: bool):
+def _flat_key_t(c: torch.Tensor, dims) -> torch.Tensor:
+    key = torch.zeros(c.shape[0], dtype=torch.int64, device=c.device)
+    for w, d in enumerate(dims):
+        key = key * int(d) + c[:, w].to(torch.int64)
+    return key
+
+
+class _ExactLayout:
+    """Every nonzero's canonical shard per mode (oracle.canonical_build at
+    the run's parameters), indexed by the sorted flattened coordinate --
+    coordinates are distinct, so per-shard multiset equality is exactly
+    "same key set, same shard and value bits per key"."""
+
+    def __init__(self, subs, v64, params):
+        L = oracle.canonical_build(subs, v64, params.dims, params.m, params.k, params.g)
+        key = np.zeros(len(v64), dtype=np.int64)
+        for w, d in enumerate(params.dims):
+            key = key * int(d) + subs[:, w]
+        perm = np.argsort(key, kind="stable")
+        self.key = key[perm]
+        self.sid = [L.sids_all[perm, n] for n in range(len(params.dims))]
+        self.vbits = v64[perm].astype(np.float32).view(np.uint32)
+        self.shard_offsets = L.shard_offsets
+        self.ss_counts = L.ss_counts
+        self.dims = params.dims
+        del L
+
+    def check(self, st, mode: int):
+        assert st.active_mode == mode
+        for n in range(len(self.dims)):
+            assert np.array_equal(st.plan.shard_offsets[n], self.shard_offsets[n]), n
+        crd = st.crd[st.active]
+        key = _flat_key_t(crd[:, :len(self.dims)], self.dims)
+        ks, perm = torch.sort(key)
+        assert np.array_equal(ks.cpu().numpy(), self.key), f"mode {mode}: nonzero set differs"
+        offs = torch.as_tensor(st.plan.shard_offsets[mode], device=st.device)
+        sid = torch.searchsorted(offs, perm, right=True) - 1
+        assert np.array_equal(sid.cpu().numpy(), self.sid[mode]), f"mode {mode}: shard membership"
+        vb = (crd[:, -1] if st.val[st.active] is None else st.val[st.active].view(torch.int32))[perm]
+        assert np.array_equal(vb.cpu().numpy().view(np.uint32), self.vbits), f"mode {mode}: values"
+
+
+class _DigestLayout:
+    """Per-shard (hash, count) of the canonical assignment, streamed in C
+    from the input records (oracle.shard_hashes), one mode at a time."""
+
+    def __init__(self, records, params):
+        self.records, self.params = records, params
+        self.cache = {}
+
+    def check(self, st, mode: int):
+        p = self.params
+        if mode not in self.cache:
+            self.cache[mode] = oracle.shard_hashes(self.records, len(p.dims), mode, p.m, p.k, p.g)
+        ss, h, c = self.cache[mode]
+        assert np.array_equal(ss, st.plan.ss_counts[mode])
+        assert np.array_equal(np.concatenate(([0], np.cumsum(c))), st.plan.shard_offsets[mode])
+        gh, gc = device_shard_digests(st, mode)
+        assert np.array_equal(gc, c), f"mode {mode}: shard fills"
+        bad = np.nonzero(gh != h)[0]
+        assert bad.size == 0, f"mode {mode}: {bad.size} of {h.size} shards differ (first {bad[:5]})"
+
+
+def _host_records(coords: torch.Tensor, vals: torch.Tensor) -> np.ndarray:
+    """(nnz, N + 1) int32 host records in input order: coordinates + value bits."""
+    N = coords.shape[1]
+    rec = np.empty((coords.shape[0], N + 1), dtype=np.int32)
+    for a in range(0, coords.shape[0], 1 << 27):
+        rec[a:a + (1 << 27), :N] = coords[a:a + (1 << 27)].cpu().numpy()
+        rec[a:a + (1 << 27), N] = vals[a:a + (1 << 27)].view(torch.int32).cpu().numpy()
+    return rec
+
+
+def _run(cfg: int, full_oracle: bool, layout: str | None = None):
     from paper_2309_09131_b200 import (DeviceFactorSet, build_device_sharded, device_params,
                                        mttkrp_mode, schedule_super_shards)
     from paper_2309_09131_b200.synth import CONFIGS, config_tensor
@@ -93,6 +176,12 @@ def _run(cfg: int, full_oracle: bool):
         from paper_2309_09131_b200.synth import zipf_records_bucketed
         rec = zipf_records_bucketed(dims, c["nnz"], seed=cfg, exponents=c["law"])
         params = device_params(dims, c["nnz"], R)
+        checker = None
+        if layout == "digest":
+            host = np.empty(tuple(rec.shape), dtype=np.int32)
+            for a in range(0, rec.shape[0], 1 << 27):
+                host[a:a + (1 << 27)] = rec[a:a + (1 << 27)].cpu().numpy()
+            checker = _DigestLayout(host, params)
         st = build_device_sharded_lean(rec, params)
         del rec
     else:
@@ -101,7 +190,12 @@ def _run(cfg: int, full_oracle: bool):
         if full_oracle:
             subs = coords.cpu().numpy().astype(np.int64)
             v64 = vals.cpu().numpy().astype(np.float64)
-        st = build_device_sharded(coords, vals, params)
+        checker = None
+        if layout == "exact":
+            checker = _ExactLayout(subs, v64, params)
+        elif layout == "digest":
+            checker = _DigestLayout(_host_records(coords, vals), params)
+        st = build_device_sharded(coords, vals, params, check_duplicates=False)
         del coords, vals
     torch.cuda.empty_cache()
     smap = schedule_super_shards(st.plan, 1)
@@ -110,6 +204,8 @@ def _run(cfg: int, full_oracle: bool):
     start = _checksum(st.crd[st.active])
     rng = np.random.default_rng(cfg)
     N = len(dims)
+    if checker is not None:
+        checker.check(st, 0)
     for n in range(N):
         _assert_in_super_shards(st, n)
         if full_oracle:
@@ -128,23 +224,27 @@ def _run(cfg: int, full_oracle: bool):
             assert cnt > 0
             assert_rel(got[torch.as_tensor(rows, device=got.device)].double().cpu().numpy(), want,
                        what=f"c{cfg} mode {n} sampled rows")
+        if checker is not None:
+            checker.check(st, (n + 1) % N)
     _assert_in_super_shards(st, 0)
     assert _checksum(st.crd[st.active]) == start, f"c{cfg}: cycle identity broken"
 
 
-def test_c2_full_every_row():
-    _run(2, full_oracle=True)
+def test_c2_full_every_row_and_exact_layout():
+    _run(2, full_oracle=True, layout="exact")
 
 
-def test_c3_full_sampled_rows():
-    _run(3, full_oracle=False)
+def test_c3_full_sampled_rows_and_shard_digests():
+    _run(3, full_oracle=False, layout="digest")
 
 
-def test_c4_full_sampled_rows():
-    _run(4, full_oracle=False)
+def test_c4_full_sampled_rows_and_shard_digests():
+    _run(4, full_oracle=False, layout="digest")
 
 
 def test_c5_full_sampled_rows():
     """3.6B nonzeros, 46 mode-0 rows of ~78M nonzeros each (heavy rows split
-    over ~9.5k chunks each, two-level K2)."""
-    _run(5, full_oracle=False)
+    over ~9.5k chunks each, two-level K2); per-shard digests with
+    FLYCOO_C5_DIGESTS=1 (host memory ~160 GB)."""
+    _run(5, full_oracle=False,
+         layout="digest" if os.environ.get("FLYCOO_C5_DIGESTS") == "1" else None)

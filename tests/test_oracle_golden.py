@@ -104,3 +104,24 @@ def test_device_order_keeps_reference_shards(name):
 def test_lpt_schedule_matches_reference():
     for case in json.loads((GOLDEN / "schedule.json").read_text()):
         assert oracle.lpt_schedule(case["counts"], case["nu"]) == case["assign"]
+
+
+@pytest.mark.parametrize("name", golden_layout_names())
+def test_streaming_shard_hashes_match_canonical_build(name):
+    """The C streaming restatement of the canonical shard assignment
+    (oracle.shard_hashes, used for c3-c5) against canonical_build's shard
+    ids on the reference-generated layouts, every mode."""
+    z = load_layout(name)
+    N = len(z["dims"])
+    L = oracle.canonical_build(z["subs"], z["vals"], z["dims"], z["m"], z["k"], int(z["g"]))
+    rec = np.zeros((L.nnz, N + 1), dtype=np.int32)
+    rec[:, :N] = z["subs"]
+    vb = z["vals"].astype(np.float32).view(np.uint32)
+    rec[:, N] = vb.view(np.int32)
+    for n in range(N):
+        nsh = int(L.ss_first_shard[n][-1])
+        want_h, want_c = oracle.shard_digests_from_ids(z["subs"], vb, L.sids_all[:, n], nsh)
+        for threads in (1, 3):
+            ss, h, c = oracle.shard_hashes(rec, N, n, z["m"], z["k"], int(z["g"]), threads=threads)
+            assert np.array_equal(ss, L.ss_counts[n])
+            assert np.array_equal(c, want_c) and np.array_equal(h, want_h), (name, n, threads)
