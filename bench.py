@@ -138,18 +138,18 @@ def describe(cfg_index: int, cfg: dict) -> str:
             f"{cfg['semantics']}-factor sweep, fp32 values/factors U(0,1)")
 
 
-def kernel_names(st, rank: int) -> list:
+def kernel_names(params, works, rank: int) -> list:
     """The K1 instance the library dispatches for each mode (mode_pass.cu
     dispatch + dispatch.cuh): the general kernel when the accumulator tile is
     not in shared memory or the shape is off the fast path; for 3-mode
     tensors the packed kernel (8-B sorted records when the two input
     coordinates fit 32 bits, else the WIDE {c_w1, c_w2} + value variant);
     otherwise the tile kernel."""
-    dims = st.params.dims
+    dims = params.dims
     N = len(dims)
     names = []
     for n in range(N):
-        w = st.mode_work(n, rank)
+        w = works[n]
         fast = (w.acc_in_smem and w.hist_rows <= 256 and 2 <= N <= 4 and rank % 4 == 0
                 and rank <= 64)
         if not fast:
@@ -332,8 +332,30 @@ def run_ours(args, rank, world, local):
         cpu_sample_n = args.cpu_sample or (nnz if nnz <= CPU_FULL_MAX else 8_000_000)
         if cpu_sample_n == nnz and not lean:
             host_copy = (coords.cpu().numpy().astype(np.int64), vals.cpu().numpy().astype(np.float64))
+    exchange = os.environ.get("FLYCOO_EXCHANGE", "p2p")
+    # N > 1 with the fused exchange: every rank builds only its slices from its
+    # block of the input (distbuild.build_partitioned) -- no rank holds the
+    # global layout; FLYCOO_GLOBAL_BUILD=1: global build, then sliced
+    partitioned = world > 1 and exchange == "p2p" and os.environ.get("FLYCOO_GLOBAL_BUILD") != "1"
     t0 = time.perf_counter()
-    if lean:
+    st = loc = None
+    if partitioned:
+        from paper_2309_09131_b200.distbuild import build_partitioned
+        lo, hi = nnz * rank // world, nnz * (rank + 1) // world
+        if lean:
+            bc = rec[lo:hi, :3].clone()
+            bv = rec[lo:hi, 3].clone().view(torch.float32)
+            del rec
+        else:
+            bc, bv = coords[lo:hi].clone(), vals[lo:hi].clone()
+            del coords, vals
+        torch.cuda.empty_cache()
+        loc = build_partitioned(bc, bv, lo, params, R=R, device=dev)
+        del bc, bv
+        torch.cuda.synchronize()
+        build_stages = {"partitioned_build": time.perf_counter() - t0}
+        plan = loc.plan
+    elif lean:
         st = build_device_sharded_lean(rec, params, device=dev)
         del rec
     else:
@@ -341,17 +363,17 @@ def run_ours(args, rank, world, local):
         st = build_device_sharded(coords, vals, params, device=dev, check_duplicates=False)
         del coords, vals
     build_s = time.perf_counter() - t0
-    build_stages = dict(st.build_stages)
-    smap = schedule_super_shards(st.plan, 1)
-    kernels = kernel_names(st, R)
+    if st is not None:
+        build_stages = dict(st.build_stages)
+        plan = st.plan
+    smap = schedule_super_shards(plan, 1)
     factors = DeviceFactorSet.random_device(dims, R, seed=1000 + args.config, device=dev)
     updated = cfg["semantics"] == "updated"
-    exchange = os.environ.get("FLYCOO_EXCHANGE", "p2p")
     dt = None
     fallback = None  # why the fused peer exchange was not used (N > 1)
     if world > 1:
-        # partitioned sweep: every rank builds the same global layout, keeps
-        # its slices + static exchange plan, and frees the rest
+        # partitioned sweep: each rank holds its slices + the static exchange
+        # plan (from the per-rank build above, or cut from a global layout)
         # exchange: "p2p" (default) = remap fused with the exchange, records
         # stored into the owners' buffers over NVLink (peer.py); "nccl" =
         # send region + all_to_all_single + unpack (dist.py)
@@ -371,7 +393,7 @@ def run_ours(args, rank, world, local):
                 return int(flag.item()) == 1
 
             try:
-                dt = PeerShardedTensor(st, world, rank)
+                dt = PeerShardedTensor(loc if partitioned else st, world, rank)
             except Exception as e:  # noqa: BLE001 -- reported, then the NCCL path
                 dt, fallback = None, f"{type(e).__name__}: {e}"[:200]
             connected = False
@@ -392,9 +414,13 @@ def run_ours(args, rank, world, local):
                       file=sys.stderr)
                 exchange = "nccl"
         if exchange != "p2p":
+            if st is None:  # the fallback slices a global layout
+                coords, vals = config_tensor(args.config, device=dev, nnz=nnz)
+                st = build_device_sharded(coords, vals, params, device=dev, check_duplicates=False)
+                del coords, vals
             dt = DistShardedTensor(st, world, rank)
         plan_s = time.perf_counter() - t0
-        del st
+        st = loc = None
         torch.cuda.empty_cache()
         ops = CudaOps()
 
@@ -508,6 +534,7 @@ def run_ours(args, rank, world, local):
     launches_per_step = sum(src.mode_work(n, R).launches + (1 if dt is not None else 0)
                             for n in range(N))
     traffic, traffic_src = measured_traffic(args.config, nnz, params)
+    kernels = kernel_names(params, [src.mode_work(n, R) for n in range(N)], R)
 
     # end to end through the public API: pinned host factors in, results out
     e2e = None
@@ -594,7 +621,10 @@ def run_ours(args, rank, world, local):
                        # build stages (CUDA events; PAPER.md:762 reports super-shard
                        # generation, Morton ordering and shard generation)
                        "build_stages_s": {k: round(v, 4) for k, v in build_stages.items()},
-                       "build": "lean (bucketed generator, layout.build_device_sharded_lean)" if lean else "regular",
+                       "build": ("partitioned (per-rank slices, distbuild.build_partitioned)"
+                                 if partitioned else
+                                 "lean (bucketed generator, layout.build_device_sharded_lean)"
+                                 if lean else "regular"),
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
                        # median over the measured sweeps of each mode pass
                        "mode_ms": [round(1e3 * statistics.median(mode_secs[n::N]), 4)

@@ -41,7 +41,8 @@ import torch.distributed as dist
 from . import _lib
 from .layout import DeviceShardedTensor, PartitionPlan, make_mode_work
 
-__all__ = ["PeerModePlan", "partition_chunks", "super_shard_owners", "peer_plans", "IpcBuffer",
+__all__ = ["PeerModePlan", "partition_chunks", "super_shard_owners", "peer_plans", "slice_bounds",
+           "IpcBuffer",
            "PeerShardedTensor", "peer_mttkrp_mode", "peer_sweep_all_modes", "PeerSweepGraph"]
 
 
@@ -122,10 +123,8 @@ def super_shard_owners(work, k: int, m: int, chunk_gpu: np.ndarray, world: int) 
     return owner
 
 
-def peer_plans(plan: PartitionPlan, slot_maps, world: int, rank: int, R: int, device):
-    """Per-mode plans of `rank` on the global single-GPU work plans (one per
-    mode, rank R).  Returns (plans, works, cap): cap = the largest element
-    slice of any GPU in any mode (record buffer rows)."""
+def _chunk_partition(plan: PartitionPlan, world: int, R: int, device):
+    """The global work plan of every mode and its chunk / element bounds per GPU."""
     N = plan.num_modes
     works, cbs = [], []
     for n in range(N):
@@ -134,6 +133,33 @@ def peer_plans(plan: PartitionPlan, slot_maps, world: int, rank: int, R: int, de
         cbs.append(partition_chunks(w.chunk_start.cpu().numpy(), world))
     starts = [w.chunk_start.cpu().numpy() for w in works]
     ebs = [starts[n][cbs[n]] for n in range(N)]
+    return works, cbs, ebs
+
+
+def slice_bounds(plan: PartitionPlan, world: int, R: int, device) -> list:
+    """Per mode, the world + 1 element bounds of the GPUs' slices (a pure
+    function of the plan: the partitioned build routes slot-map entries and
+    records with it, distbuild.build_partitioned)."""
+    return [[int(x) for x in eb] for eb in _chunk_partition(plan, world, R, device)[2]]
+
+
+def _slot_slice(src, n: int, lo: int, hi: int) -> torch.Tensor:
+    """[lo, hi) of mode n's global slot map from a DeviceShardedTensor, a
+    LocalLayout (its own slice) or a plain list of slot maps."""
+    if hasattr(src, "slot_slice"):
+        return src.slot_slice(n, lo, hi)
+    maps = src if isinstance(src, (list, tuple)) else src.slot_maps
+    return maps[n][lo:hi]
+
+
+def peer_plans(plan: PartitionPlan, src, world: int, rank: int, R: int, device):
+    """Per-mode plans of `rank` on the global single-GPU work plans (one per
+    mode, rank R); `src` provides the global slot maps (a DeviceShardedTensor)
+    or this rank's slices of them (distbuild.LocalLayout).  Returns (plans,
+    works, cap): cap = the largest element slice of any GPU in any mode
+    (record buffer rows)."""
+    N = plan.num_modes
+    works, cbs, ebs = _chunk_partition(plan, world, R, device)
     cap = max(int(eb[p + 1] - eb[p]) for eb in ebs for p in range(world))
     plans = []
     for n in range(N):
@@ -153,7 +179,7 @@ def peer_plans(plan: PartitionPlan, slot_maps, world: int, rank: int, R: int, de
         t = lambda a, dt=torch.int64: torch.from_numpy(np.ascontiguousarray(a)).to(dt).to(device)
         plans.append(PeerModePlan(
             c_lo, c_hi, e_lo, e_hi, lo_ss[rank], lo_ss[rank + 1],
-            slot_maps[n][e_lo:e_hi].to(torch.int32).clone().to(device),
+            _slot_slice(src, n, e_lo, e_hi).to(torch.int32).clone().to(device),
             [int(x) for x in ebs[(n + 1) % N]], rows,
             t(owner[cs[c_lo:c_hi]], torch.int32), t(r1), t(r2)))
     return plans, works, max(cap, 1)
@@ -209,8 +235,11 @@ class PeerShardedTensor:
     the single-GPU parity test of the peer-store kernel path).  `R` is the
     factor rank the work plans are built for (default: the params' rank)."""
 
-    def __init__(self, st: DeviceShardedTensor, world: int, rank: int, group=None,
+    def __init__(self, st, world: int, rank: int, group=None,
                  ipc: bool = True, R: int | None = None):
+        """`st`: the global DeviceShardedTensor (sliced here), or this rank's
+        distbuild.LocalLayout (the partitioned build: no rank holds the
+        whole layout)."""
         if world > 8:
             raise ValueError("the fused exchange maps at most 8 peers")
         self.plan = st.plan
@@ -218,19 +247,23 @@ class PeerShardedTensor:
         self.device = st.device
         self.num_modes = st.num_modes
         self.R = int(R if R is not None else st.plan.params.rank)
-        self.plans, self.works, self.cap = peer_plans(st.plan, st.slot_maps, world, rank,
-                                                      self.R, st.device)
-        cw = st.crd[0].shape[1]
+        self.plans, self.works, self.cap = peer_plans(st.plan, st, world, rank, self.R, st.device)
+        p0 = self.plans[0]
+        if hasattr(st, "records_slice"):
+            crd0, val0 = st.records_slice(p0.e_lo, p0.e_hi)
+        else:
+            crd0 = st.crd[st.active][p0.e_lo:p0.e_hi]
+            val0 = None if st.val[st.active] is None else st.val[st.active][p0.e_lo:p0.e_hi]
+        cw = crd0.shape[1]
         self.cw = cw
-        emb = st.val[0] is None
+        emb = val0 is None
         self._bufs = []
         self.crd = [self._alloc((self.cap, cw), torch.int32) for _ in range(2)]
         self.val = [None, None] if emb else [self._alloc((self.cap,), torch.float32)
                                             for _ in range(2)]
-        p0 = self.plans[0]
-        self.crd[0][:p0.count] = st.crd[st.active][p0.e_lo:p0.e_hi]
+        self.crd[0][:p0.count] = crd0
         if not emb:
-            self.val[0][:p0.count] = st.val[st.active][p0.e_lo:p0.e_hi]
+            self.val[0][:p0.count] = val0
         # partial tiles, indexed by the global partial id: peers write the
         # partials of super-shards this GPU owns into it (one buffer for all
         # modes: a mode's partials are reduced before any GPU starts the next)

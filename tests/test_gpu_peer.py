@@ -135,13 +135,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, result, sync):
+def _ipc_worker(rank, world, port, result, sync, distinct=False):
     os.environ["FLYCOO_PEER_SYNC"] = sync
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        # distinct: one GPU per rank, the records and rows cross NVLink
+        torch.cuda.set_device(rank if distinct else 0)
         from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode, schedule_super_shards
         from paper_2309_09131_b200.peer import PeerShardedTensor, peer_sweep_all_modes
         for N in (3, 4):
@@ -196,5 +197,19 @@ def test_peer_exchange_processes_ipc(world, sync):
     ctx = mp.get_context("spawn")
     result = ctx.Manager().dict()
     mp.start_processes(_ipc_worker, args=(world, _free_port(), result, sync), nprocs=world,
+                       join=True, start_method="spawn")
+    assert sorted(result.keys()) == list(range(world))
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (one per rank)")
+@pytest.mark.parametrize("sync", ["device", "host"])
+def test_peer_exchange_multi_gpu_nvlink(sync):
+    """One process per GPU (up to 4): the fused exchange over real NVLink
+    peer mappings; slices and factors bit-exact against the single-GPU sweep
+    after every chained sweep and graph replay."""
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    result = ctx.Manager().dict()
+    mp.start_processes(_ipc_worker, args=(world, _free_port(), result, sync, True), nprocs=world,
                        join=True, start_method="spawn")
     assert sorted(result.keys()) == list(range(world))

@@ -201,3 +201,30 @@ def test_lean_build_rejects_unsupported_layouts():
     with pytest.raises(ValueError, match="Morton key"):
         build_device_sharded_lean(rec, device_params((1 << 20, 1 << 20, 1 << 20), 10, 8, m=[1, 1, 1]),
                                   device="cpu")
+
+
+def _header_params(name: str) -> list:
+    """Parameter types of a declaration in include/flycoo.h (comments stripped)."""
+    hdr = (ROOT / "include" / "flycoo.h").read_text()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    m = re.search(rf"\b{name}\((.*?)\);", hdr, re.S)
+    assert m, name
+    return [p.strip() for p in m.group(1).split(",")]
+
+
+def test_reference_binding_matches_header():
+    """INTEGRATION.md section 2's ctypes binding (tests/reference_binding.py)
+    declares one ctypes type per C parameter of fc_mode_worker, with the
+    integer widths of the header."""
+    import ctypes
+    import reference_binding as rb
+    params = _header_params("fc_mode_worker")
+    assert len(params) == len(rb.MODE_WORKER_ARGTYPES)
+    for p, t in zip(params, rb.MODE_WORKER_ARGTYPES):
+        if "*" in p:
+            assert t is ctypes.c_void_p, p
+        elif p.startswith("int64_t"):
+            assert t is ctypes.c_int64, p
+        else:
+            assert p.startswith("int ") and t is ctypes.c_int, p
+    assert rb.lib().fc_version() == 1
