@@ -19,6 +19,7 @@
  * like numba/numpy do (no FMA contraction), which is what makes the oracle
  * bit-identical to the reference on the golden fixtures.
  */
+#include <immintrin.h>
 #include <pthread.h>
 #include <stdatomic.h>
 #include <stdint.h>
@@ -290,6 +291,7 @@ typedef struct {
   int nmodes, mode;
   const int64_t *m;
   int widths[16], maxw, total;
+  uint64_t deposit[16];             /* key bit positions of every mode (morton.py:20-44) */
   const uint32_t *ids; const int64_t *ss_off; const int64_t *first; int64_t g;
   int64_t nss;
   _Atomic int64_t *next;            /* work queue over super-shards (largest first) */
@@ -298,15 +300,12 @@ typedef struct {
   int err;
 } orc_hash_job_t;
 
+/* the same key as orc_morton: bit b of mode w goes to the position the
+ * level-major interleave gives it, here one bit-deposit per mode */
 static uint64_t orc_morton_row(const orc_hash_job_t *J, const int32_t *c) {
   uint64_t l = 0;
-  int pos = 0;
-  for (int b = 0; b < J->maxw; ++b)
-    for (int w = 0; w < J->nmodes; ++w) {
-      if (b >= J->widths[w]) continue;
-      l |= ((uint64_t)(c[w] / J->m[w]) >> b & 1u) << pos;
-      ++pos;
-    }
+  for (int w = 0; w < J->nmodes; ++w)
+    l |= _pdep_u64((uint64_t)(c[w] / J->m[w]), J->deposit[w]);
   return l;
 }
 
@@ -371,6 +370,92 @@ static int orc_cmp_desc(const void *a, const void *b) {
   return (x[1] > y[1]) - (x[1] < y[1]);
 }
 
+/* One big super-shard processed by all threads: Morton keys, a parallel
+ * stable LSD radix sort (per-thread digit histograms, thread-ordered
+ * offsets, in-order scatter), then per-shard digests with atomic wrapping
+ * adds (sums commute, so the digests are deterministic). */
+typedef struct {
+  const orc_hash_job_t *J;
+  int64_t lo, n;                     /* super-shard s: elements ids[lo, lo + n) */
+  int64_t s;
+  uint64_t *k0, *k1;
+  uint32_t *i0, *i1;
+  int64_t *hist;                     /* [threads][2048] */
+  pthread_barrier_t *bar;
+  int t, T;
+} orc_big_t;
+
+static void *orc_big_run(void *arg) {
+  orc_big_t *B = (orc_big_t *)arg;
+  const orc_hash_job_t *J = B->J;
+  const int64_t a = B->n * B->t / B->T, b = B->n * (B->t + 1) / B->T;
+  for (int64_t r = a; r < b; ++r) {
+    const uint32_t id = J->ids[B->lo + r];
+    B->i0[r] = id;
+    B->k0[r] = orc_morton_row(J, J->coords + (int64_t)id * J->cs);
+  }
+  uint64_t *ka = B->k0, *kb = B->k1;
+  uint32_t *ia = B->i0, *ib = B->i1;
+  int64_t *h = B->hist + (int64_t)B->t * 2048;
+  for (int sh = 0; sh < J->total; sh += 11) {
+    pthread_barrier_wait(B->bar);
+    memset(h, 0, sizeof(int64_t) * 2048);
+    for (int64_t r = a; r < b; ++r) h[(ka[r] >> sh) & 2047]++;
+    pthread_barrier_wait(B->bar);
+    if (B->t == 0) {                 /* offsets: digit-major, thread order inside a digit */
+      int64_t run = 0;
+      for (int d = 0; d < 2048; ++d)
+        for (int t = 0; t < B->T; ++t) {
+          int64_t *c = B->hist + (int64_t)t * 2048 + d;
+          const int64_t x = *c;
+          *c = run;
+          run += x;
+        }
+    }
+    pthread_barrier_wait(B->bar);
+    for (int64_t r = a; r < b; ++r) {
+      const int64_t t = h[(ka[r] >> sh) & 2047]++;
+      kb[t] = ka[r];
+      ib[t] = ia[r];
+    }
+    uint64_t *tk = ka; ka = kb; kb = tk;
+    uint32_t *ti = ia; ia = ib; ib = ti;
+  }
+  pthread_barrier_wait(B->bar);
+  for (int64_t r = a; r < b; ++r) {
+    const int64_t id = ia[r];
+    const int64_t sh = J->first[B->s] + r / J->g;
+    __atomic_fetch_add(&J->hash[sh], orc_elem_hash(J->coords + id * J->cs, J->nmodes,
+                                                    J->vbits[id * J->vs]), __ATOMIC_RELAXED);
+    __atomic_fetch_add(&J->count[sh], 1, __ATOMIC_RELAXED);
+  }
+  return NULL;
+}
+
+static int orc_big_super_shard(const orc_hash_job_t *J, int64_t s, int T) {
+  const int64_t lo = J->ss_off[s], n = J->ss_off[s + 1] - lo;
+  uint64_t *k0 = (uint64_t *)malloc((size_t)n * 8), *k1 = (uint64_t *)malloc((size_t)n * 8);
+  uint32_t *i0 = (uint32_t *)malloc((size_t)n * 4), *i1 = (uint32_t *)malloc((size_t)n * 4);
+  int64_t *hist = (int64_t *)malloc(sizeof(int64_t) * 2048 * T);
+  pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * T);
+  orc_big_t *B = (orc_big_t *)malloc(sizeof(orc_big_t) * T);
+  int rc = 0;
+  if (!k0 || !k1 || !i0 || !i1 || !hist || !tid || !B) {
+    rc = -1;
+  } else {
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)T);
+    for (int t = 0; t < T; ++t) {
+      B[t] = (orc_big_t){J, lo, n, s, k0, k1, i0, i1, hist, &bar, t, T};
+      pthread_create(&tid[t], NULL, orc_big_run, &B[t]);
+    }
+    for (int t = 0; t < T; ++t) pthread_join(tid[t], NULL);
+    pthread_barrier_destroy(&bar);
+  }
+  free(k0); free(k1); free(i0); free(i1); free(hist); free(tid); free(B);
+  return rc;
+}
+
 int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, int64_t vs,
                      int64_t nnz, int nmodes, int mode, const int64_t *m, const int64_t *k,
                      int64_t g, int threads, int64_t *ss_counts, uint64_t *hash,
@@ -386,6 +471,12 @@ int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, i
     if (J.widths[w] > J.maxw) J.maxw = J.widths[w];
   }
   if (J.total > 64) return -2;
+  {
+    int pos = 0;
+    for (int b = 0; b < J.maxw; ++b)
+      for (int w = 0; w < nmodes; ++w)
+        if (b < J.widths[w]) J.deposit[w] |= 1ull << pos++;
+  }
   const int64_t K = k[mode];
   /* super-shard of every element, counts (layout.py:487) */
   memset(ss_counts, 0, sizeof(int64_t) * K);
@@ -426,6 +517,17 @@ int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, i
   _Atomic int64_t next = 0;
   J.ids = ids; J.ss_off = off; J.first = first; J.nss = K; J.next = &next; J.queue = queue;
   J.hash = hash; J.count = count;
+  /* super-shards holding more than 1/(2 threads) of the elements (Zipf
+   * heads: c4's first super-shard) are sorted by all threads together */
+  int64_t nbig = 0;
+  while (threads > 1 && nbig < K && ss_counts[queue[nbig]] * 2 * threads > nnz) {
+    if (orc_big_super_shard(&J, queue[nbig], threads) != 0) {
+      free(off); free(first); free(fill); free(queue); free(ids);
+      return -1;
+    }
+    ++nbig;
+  }
+  next = nbig;
   /* the largest super-shards go first: one thread holds the largest scratch,
    * the others the size of the (threads)-th largest */
   if (threads > K) threads = (int)(K > 0 ? K : 1);
