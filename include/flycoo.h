@@ -64,11 +64,6 @@ int fc_tile_elems(void);             /* elements per CTA tile (fixed)     */
  * pack = 8-byte sorted records for 3-mode tensors whose input coordinates
  * fit 32 bits, pack_wide = the {c_w1, c_w2} + value variant otherwise. */
 int fc_set_kernel_variant(int pack, int pack_wide);
-/* L2 budget (bytes; 0 = off, the default; FLYCOO_L2_HOT_MB sets it at load)
- * for the factor-row gathers of the WIDE packed kernel: the first
- * bytes / ((N-1) * 4R) rows of every input factor load with evict_last, the
- * rest with evict_first. */
-int fc_set_l2_hot_bytes(int64_t bytes);
 /* Row capacity of a "direct" chunk merging consecutive small super-shards
  * (fast path only; returns m when merging is not supported). */
 int64_t fc_chunk_rows_max(int nmodes, int rank, int64_t m);

@@ -32,7 +32,6 @@ _SIGS = {
     "fc_smem_acc_rows_max": (_i64, [_int]),
     "fc_tile_elems": (_int, []),
     "fc_set_kernel_variant": (_int, [_int, _int]),
-    "fc_set_l2_hot_bytes": (_int, [_i64]),
     "fc_chunk_rows_max": (_i64, [_int, _int, _i64]),
     "fc_mode_worker": (_int, [
         _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val

@@ -15,12 +15,7 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     const KernelVariant &kv = kernel_variant();
     if (a.pack_shift > 0 && kv.pack) return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
     // wider coordinates: {c_w1, c_w2} + value array, rows from the bins
-    if (a.pack_shift == 0 && kv.pack_wide) {
-      // factors beyond L2 with an L2 budget: the evict_last / evict_first gathers
-      if (!PEER && RT > 0 && a.hot_rows[MODE == 0 ? 1 : 0] > 0)
-        return launch_pack<MODE, LPG, RT, PEER, true, true>(a, nchunks, st);
-      return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
-    }
+    if (a.pack_shift == 0 && kv.pack_wide) return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
   return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
 }

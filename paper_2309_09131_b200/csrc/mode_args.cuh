@@ -58,11 +58,6 @@ struct ModeArgs {
   // super-shard whose chunks span GPUs gets its partial tiles written into
   // the owner's workspace, which reduces them after a barrier.
   const int32_t *chunk_owner;
-  // L2 policy for factor-row gathers (fc_set_l2_hot_bytes; 0 = default
-  // policy): rows below hot_rows[w] of input factor w load with evict_last,
-  // the rest with evict_first, so the Zipf-hot rows stay resident in L2
-  // while the cold tail and the record stream pass through
-  int64_t hot_rows[8];
 };
 
 // Partial-tile workspace of chunk c (indexed by the global partial id).
@@ -155,27 +150,6 @@ __device__ __forceinline__ int chunk_row_count(const ModeArgs &a, int64_t c, int
   return (int)min64(r, a.out_rows - row0);
 }
 
-// L2 eviction-priority policies (createpolicy) and a read-only 16-B load
-// carrying one: the policy is a register operand, so lanes of one warp can
-// load with different priorities in one instruction
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ float4 ldg_policy(const float4 *p, uint64_t pol) {
-  float4 r;
-  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-      : "l"(p), "l"(pol));
-  return r;
-}
-
 __device__ __forceinline__ int4 ld_stream_v4(const int4 *p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -262,7 +236,6 @@ int fast_dispatch_peer_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 struct KernelVariant {
   bool pack = true;
   bool pack_wide = true;
-  int64_t l2_hot_bytes = 0;  // budget of evict_last factor rows (0: off)
 };
 KernelVariant &kernel_variant();
 

@@ -478,8 +478,6 @@ static KernelVariant variant_from_env() {
   const char *w = getenv("FLYCOO_PACK_WIDE");
   v.pack = !(p && strcmp(p, "0") == 0);
   v.pack_wide = !(w && strcmp(w, "0") == 0);
-  const char *h = getenv("FLYCOO_L2_HOT_MB");
-  v.l2_hot_bytes = h ? (int64_t)(atof(h) * 1e6) : 0;
   return v;
 }
 static KernelVariant g_variant = variant_from_env();
@@ -492,11 +490,6 @@ using namespace fc;
 extern "C" {
 
 int64_t fc_smem_acc_rows_max(int rank) { return fc::smem_acc_rows_max(rank); }
-
-int fc_set_l2_hot_bytes(int64_t bytes) {
-  fc::kernel_variant().l2_hot_bytes = bytes > 0 ? bytes : 0;
-  return FC_OK;
-}
 
 int fc_set_kernel_variant(int pack, int pack_wide) {
   fc::kernel_variant().pack = pack != 0;
@@ -608,12 +601,6 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
   a.counters = counters;
   a.peers = peers;
   a.chunk_owner = chunk_owner;
-  for (int w = 0; w < 8; ++w) a.hot_rows[w] = 0;
-  if (kernel_variant().l2_hot_bytes > 0 && dims && nmodes > 1) {
-    const int64_t per = kernel_variant().l2_hot_bytes / (int64_t)(nmodes - 1) / (4 * (int64_t)rank);
-    for (int w = 0; w < nmodes && w < 8; ++w)
-      if (w != mode) a.hot_rows[w] = per < dims[w] ? per : dims[w];
-  }
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
   if (acc_in_smem && nred1 > 0) {

@@ -45,7 +45,7 @@ struct PackPlan {
   }
 };
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, bool L2POL = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const __grid_constant__ ModeArgs a) {
   using PP = PackPlan<LPG, WIDE>;
   constexpr int G = PP::G;
@@ -326,23 +326,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       const float *f2b = a.fac[W2] + col;
       const uint32_t rstride = (uint32_t)(RT > 0 ? RT : R);
       // q = {packed coordinates, value bits} or, WIDE, {c_w1, c_w2} (+ s_sval)
-      // WIDE (factors larger than L2): hot rows evict_last, the cold tail
-      // evict_first, when an L2 budget is set (a.hot_rows)
-      constexpr bool policy = WIDE && L2POL;
-      const uint64_t pol_last = policy ? l2_policy_evict_last() : 0;
-      const uint64_t pol_first = policy ? l2_policy_evict_first() : 0;
       auto prod = [&](const uint2 &q, f32x4p &pr) {
         const uint32_t c1 = WIDE ? q.x : q.x >> shift, c2 = WIDE ? q.y : q.x & lowmask;
-        const float4 *p1 = reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride);
-        const float4 *p2 = reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride);
-        f32x4p f1, f2;
-        if constexpr (policy) {
-          f1 = f4p(ldg_policy(p1, (int64_t)c1 < a.hot_rows[W1] ? pol_last : pol_first));
-          f2 = f4p(ldg_policy(p2, (int64_t)c2 < a.hot_rows[W2] ? pol_last : pol_first));
-        } else {
-          f1 = f4p(__ldg(p1));
-          f2 = f4p(__ldg(p2));
-        }
+        const f32x4p f1 = f4p(__ldg(reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride)));
+        const f32x4p f2 = f4p(__ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride)));
         pr.lo = f2_mul(f1.lo, f2.lo);
         pr.hi = f2_mul(f1.hi, f2.hi);
       };
@@ -425,10 +412,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 }
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, bool L2POL = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = PackPlan<LPG, WIDE>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE, L2POL>;
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

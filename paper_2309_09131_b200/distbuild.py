@@ -176,7 +176,8 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
     for n in range(N):
         sb = _ss_ranges(counts[n], world)
         ss_bounds.append(sb)
-        dest = torch.searchsorted(torch.as_tensor(sb[1:-1], device=dev), iv[:, n], right=True)
+        dest = torch.searchsorted(torch.as_tensor(sb[1:-1], device=dev), iv[:, n].contiguous(),
+                                  right=True)
         exch.append(_Exchange(dest, world, group, host))
 
     # 2. canonical shard ids (layout.py:484-492)

@@ -247,7 +247,7 @@ def _explain(dims, model: _Model, gs) -> str:
 
 
 def _auto_rows(dim: int, nnz: int, rank: int) -> int:
-    """Super-shard height of one mode (measured on c2-c4, profiles/r1_kernel_experiments.md):
+    """Super-shard height of one mode (measured on c2-c4, profiles/round1/r1_kernel_experiments.md):
     a 4 KB accumulator tile when super-shards stay large (>= 64k nonzeros: fewer rows per
     2048-element tile -> fewer segments, fewer ballot rounds) or become so sparse that
     <= 4k nonzeros share an 8 KB tile's rows (direct chunks: rows complete inside one tile);

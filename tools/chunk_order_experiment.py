@@ -7,7 +7,7 @@ of the Morton range of many super-shards -- and gather the same region of
 the input factors.  Outputs are unchanged (partial tiles are indexed by id).
 Needs an experiment build exposing fc_exp_set_chunk_order (a launch-order
 array read by the kernels as chunk = order[blockIdx.x]); it was measured
-and removed (no gain, see profiles/r1_kernel_experiments.md).
+and removed (no gain, see profiles/round1/r1_kernel_experiments.md).
 
 usage: FLYCOO_LIB=libflycoo_ord.so python tools/chunk_order_experiment.py [config]
 """
