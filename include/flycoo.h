@@ -43,6 +43,8 @@ extern "C" {
 #define FC_FLAG_ROW_OUTSIDE_SS 2  /* element's output row not in its chunk's
                                      super-shard: buffer not ordered for mode */
 #define FC_FLAG_SHARD_OVERFLOW 4  /* cursor strategy: shard fill exceeded   */
+#define FC_FLAG_INDEX_CHECK 8     /* checked build (FC_DEVICE_CHECKS) only: a
+                                     shared/global index outside its tile  */
 
 /* Element record layout in HBM ("crd" words are int32, 16-B aligned rows):
  *   N <= 3 : 4 words  {c0, c1, c2, bits(value)}   (N = 2: word 2 is 0)

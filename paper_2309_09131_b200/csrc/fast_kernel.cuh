@@ -284,12 +284,15 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         for (int b = 0; b < 8; ++b) round(b);
       }
       const unsigned grp = k >= 0 ? peers : (1u << lane);
-      // the group leader reserves the run (a warp's shared atomics to one
-      // address execute in issue order: stable) and broadcasts its base
+      // the group leader reserves the run and broadcasts its base
       const int leader = __ffs(grp) - 1;
       int old = 0;
       if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
       old = __shfl_sync(0xffffffffu, old, leader);
+      // the next item's leader may be another lane: __syncwarp orders this
+      // item's shared atomics before the next item's (memory-model order,
+      // not only the warp's in-order issue), keeping the ranks stable
+      __syncwarp();
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     __syncthreads();
@@ -332,6 +335,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       if (x >= 0) {
         const int k = x & 255;
         const int pos = wh[k] + (x >> 8);
+        FC_DCHECK(a, k < rows && pos >= 0 && pos < cnt);
         set_comp<MODE>(rec[j], irow0 + k);
         s_sorted[phys(pos)] = rec[j];
         if (!EMB) s_sval[phys(pos)] = rv[j];
@@ -364,6 +368,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
           if (lg == 0) s_bnd_row[2 * gi] = cur - irow0;
           if (col_ok) VecT<4>::store(s_bnd + (2 * gi) * R + col, acc);
         } else if (col_ok) {
+          FC_DCHECK(a, cur - irow0 >= 0 && cur - irow0 < rows && cur < a.out_rows);
           if (direct) {  // the whole row is this segment
             VecT<4>::store(out_rows + (cur - irow0) * R + col, acc);
             return;
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       for (int t = warp; t < G; t += kFWarps) {
         const int row = s_bnd_row[2 * t + 1];
         if (row < 0) continue;
+        FC_DCHECK(a, row < rows);
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
           const int c = q * 32 + lane;

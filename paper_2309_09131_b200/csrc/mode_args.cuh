@@ -60,6 +60,20 @@ struct ModeArgs {
   const int32_t *chunk_owner;
 };
 
+// Checked build (make CHECKED=1 -> libflycoo_checked.so, FC_DEVICE_CHECKS):
+// every shared-tile and output-row index is tested and a miss raises
+// FC_FLAG_INDEX_CHECK in the flag word (no trap), which the host turns into
+// an exception -- the bounds evidence in place of compute-sanitizer, which
+// is closed on this pool.  Compiled out of the product library.
+#ifdef FC_DEVICE_CHECKS
+#define FC_DCHECK(a, cond)                                                 \
+  do {                                                                     \
+    if (!(cond)) atomicOr((a).flags, FC_FLAG_INDEX_CHECK);                 \
+  } while (0)
+#else
+#define FC_DCHECK(a, cond) do { } while (0)
+#endif
+
 // Partial-tile workspace of chunk c (indexed by the global partial id).
 __device__ __forceinline__ float *partial_ws(const ModeArgs &a, int64_t c) {
   return a.chunk_owner ? a.peers.part_ws[a.chunk_owner[c]] : a.part_ws;

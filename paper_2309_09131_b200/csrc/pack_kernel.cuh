@@ -181,9 +181,8 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     } else {
     // stable per-warp counting: the leader of each equal-row group reserves
     // the group's run with one shared atomic (returns the old count) and
-    // broadcasts it; a warp's shared atomics to one address execute in issue
-    // order, so runs are ordered by (item j, lane) as before -- without a
-    // load / store / syncwarp chain per item
+    // broadcasts it; a __syncwarp per item orders the items' atomics, so runs
+    // are ordered by (item j, lane)
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int k = key_of(rec[j]);
@@ -211,6 +210,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       int old = 0;
       if (k >= 0 && lane == leader) old = atomicAdd(wh + k, __popc(grp));
       old = __shfl_sync(0xffffffffu, old, leader);
+      // the next item's leader may be another lane: __syncwarp orders this
+      // item's shared atomics before the next item's (memory-model order,
+      // not only the warp's in-order issue), keeping the ranks stable
+      __syncwarp();
       set_comp<MODE>(rec[j], k >= 0 ? (((old + __popc(grp & lt_mask)) << 8) | k) : -1);
     }
     }
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (x >= 0) {
         const int k = x & 255;
         const int pos = wh[k] + (x >> 8);
+        FC_DCHECK(a, k < rows && pos >= 0 && pos < cnt);
         if constexpr (WIDE) {
           s_sorted[phys(pos)] = make_uint2((uint32_t)comp<W1>(rec[j]), (uint32_t)comp<W2>(rec[j]));
           s_sval[phys(pos)] = __int_as_float(rec[j].w);
@@ -297,6 +301,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
           if (lg == 0) s_bnd_row[2 * gi] = cur;
           if (col_ok) put(s_bnd + (2 * gi) * R + col, acc);
         } else if (col_ok) {
+          FC_DCHECK(a, cur >= 0 && cur < rows && row0 + cur < a.out_rows);
           if (direct) {
             put(out_rows + cur * R + col, acc);
             return;
@@ -387,6 +392,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       for (int t = warp; t < G; t += kFWarps) {
         const int row = s_bnd_row[2 * t + 1];
         if (row < 0) continue;
+        FC_DCHECK(a, row < rows);
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
           const int c = q * 32 + lane;

@@ -38,6 +38,7 @@ REMAP_STRATEGIES = ("slot", "cursor")
 FLAG_SLOT_RANGE = 1
 FLAG_ROW_OUTSIDE_SS = 2
 FLAG_SHARD_OVERFLOW = 4
+FLAG_INDEX_CHECK = 8  # checked build only (FC_DEVICE_CHECKS)
 
 
 class ShardOverflowError(RuntimeError):
@@ -160,6 +161,8 @@ def check_errors(st: DeviceShardedTensor, next_mode: int | None = None) -> None:
     flags = int(stat[1]) & 0xFFFFFFFF
     expected = st._expected
     st.reset_checks()
+    if flags & FLAG_INDEX_CHECK:
+        raise RuntimeError("a kernel index check failed (checked build, FC_DEVICE_CHECKS)")
     if flags & FLAG_ROW_OUTSIDE_SS:
         raise BufferOrderError("an element's output row lies outside its super-shard: the active "
                                "buffer is not ordered for this mode")
