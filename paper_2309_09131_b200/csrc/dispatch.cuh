@@ -13,19 +13,9 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   if constexpr (NM == 3) {
     // 8-byte sorted records when the two input coordinates fit 32 bits
     const KernelVariant &kv = kernel_variant();
-    if (a.pack_shift > 0 && kv.pack) {
-      if constexpr (!PEER && RT > 0) {
-        if (a.tex[MODE == 2 ? 1 : 2]) return launch_pack<MODE, LPG, RT, false, false, true>(a, nchunks, st);
-      }
-      return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
-    }
+    if (a.pack_shift > 0 && kv.pack) return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
     // wider coordinates: {c_w1, c_w2} + value array, rows from the bins
-    if (a.pack_shift == 0 && kv.pack_wide) {
-      if constexpr (!PEER && RT > 0) {
-        if (a.tex[MODE == 2 ? 1 : 2]) return launch_pack<MODE, LPG, RT, false, true, true>(a, nchunks, st);
-      }
-      return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
-    }
+    if (a.pack_shift == 0 && kv.pack_wide) return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
   return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
 }

@@ -58,9 +58,6 @@ struct ModeArgs {
   // super-shard whose chunks span GPUs gets its partial tiles written into
   // the owner's workspace, which reduces them after a barrier.
   const int32_t *chunk_owner;
-  // texture objects (linear float4 textures) over the input factors, for
-  // the packed kernel's TEX-path gathers (0 = not created)
-  unsigned long long tex[8];
 };
 
 // Checked build (make CHECKED=1 -> libflycoo_checked.so, FC_DEVICE_CHECKS):
@@ -253,7 +250,6 @@ int fast_dispatch_peer_n4(const ModeArgs &a, int64_t nchunks, cudaStream_t st);
 struct KernelVariant {
   bool pack = true;
   bool pack_wide = true;
-  bool tex = false;  // packed kernel: second input factor through the texture path
 };
 KernelVariant &kernel_variant();
 

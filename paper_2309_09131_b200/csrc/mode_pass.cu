@@ -478,8 +478,6 @@ static KernelVariant variant_from_env() {
   const char *w = getenv("FLYCOO_PACK_WIDE");
   v.pack = !(p && strcmp(p, "0") == 0);
   v.pack_wide = !(w && strcmp(w, "0") == 0);
-  const char *t = getenv("FLYCOO_TEX");
-  v.tex = t && strcmp(t, "1") == 0;
   return v;
 }
 static KernelVariant g_variant = variant_from_env();
@@ -492,41 +490,6 @@ using namespace fc;
 extern "C" {
 
 int64_t fc_smem_acc_rows_max(int rank) { return fc::smem_acc_rows_max(rank); }
-
-// Linear float4 texture object over a factor matrix, cached per (pointer,
-// size): the same allocation gets the same object on every launch (graph
-// replays, repeated sweeps); an entry is only used while the caller passes
-// that pointer, i.e. while the memory is live.  0 when the texture would
-// exceed the linear-texture width (2^27 texels).
-static cudaTextureObject_t factor_texture(const float *p, int64_t floats) {
-  struct Entry { const float *p; int64_t n; cudaTextureObject_t t; };
-  static Entry cache[64];
-  static int used = 0;
-  if (!p || floats <= 0 || floats % 4 || floats / 4 > (1ll << 27)) return 0;
-  for (int i = 0; i < used; ++i)
-    if (cache[i].p == p && cache[i].n == floats) return cache[i].t;
-  cudaResourceDesc rd = {};
-  rd.resType = cudaResourceTypeLinear;
-  rd.res.linear.devPtr = const_cast<float *>(p);
-  rd.res.linear.desc = cudaCreateChannelDesc<float4>();
-  rd.res.linear.sizeInBytes = (size_t)floats * 4;
-  cudaTextureDesc td = {};
-  td.readMode = cudaReadModeElementType;
-  cudaTextureObject_t t = 0;
-  if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  Entry e{p, floats, t};
-  if (used < 64) {
-    cache[used++] = e;
-  } else {  // evict the oldest
-    cudaDestroyTextureObject(cache[0].t);
-    for (int i = 1; i < 64; ++i) cache[i - 1] = cache[i];
-    cache[63] = e;
-  }
-  return t;
-}
 
 int fc_set_kernel_variant(int pack, int pack_wide) {
   fc::kernel_variant().pack = pack != 0;
@@ -638,10 +601,6 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
   a.counters = counters;
   a.peers = peers;
   a.chunk_owner = chunk_owner;
-  for (int w = 0; w < 8; ++w) a.tex[w] = 0;
-  if (kernel_variant().tex && nmodes == 3 && dims && acc_in_smem)
-    for (int w = 0; w < nmodes; ++w)
-      if (w != mode) a.tex[w] = factor_texture(factors[w], dims[w] * (int64_t)rank);
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
   if (acc_in_smem && nred1 > 0) {

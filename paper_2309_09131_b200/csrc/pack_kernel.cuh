@@ -45,7 +45,7 @@ struct PackPlan {
   }
 };
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, bool TEX = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const __grid_constant__ ModeArgs a) {
   using PP = PackPlan<LPG, WIDE>;
   constexpr int G = PP::G;
@@ -331,16 +331,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       const float *f2b = a.fac[W2] + col;
       const uint32_t rstride = (uint32_t)(RT > 0 ? RT : R);
       // q = {packed coordinates, value bits} or, WIDE, {c_w1, c_w2} (+ s_sval)
-      // TEX: the second input factor's rows through the texture path (its
-      // own request queue beside the LSU path)
-      const cudaTextureObject_t t2 = TEX ? a.tex[W2] : 0;
-      const int tlg = TEX ? lg : 0;
       auto prod = [&](const uint2 &q, f32x4p &pr) {
         const uint32_t c1 = WIDE ? q.x : q.x >> shift, c2 = WIDE ? q.y : q.x & lowmask;
         const f32x4p f1 = f4p(__ldg(reinterpret_cast<const float4 *>(f1b + (uint64_t)c1 * rstride)));
-        f32x4p f2;
-        if constexpr (TEX) f2 = f4p(tex1Dfetch<float4>(t2, (int)(c2 * (RT / 4) + tlg)));
-        else f2 = f4p(__ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride)));
+        const f32x4p f2 = f4p(__ldg(reinterpret_cast<const float4 *>(f2b + (uint64_t)c2 * rstride)));
         pr.lo = f2_mul(f1.lo, f2.lo);
         pr.hi = f2_mul(f1.hi, f2.hi);
       };
@@ -424,10 +418,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 }
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, bool TEX = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
 int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = PackPlan<LPG, WIDE>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE, TEX>;
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
