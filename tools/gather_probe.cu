@@ -143,3 +143,75 @@ extern "C" float gather_probe_tma(const uint2 *idx, int64_t n, const float *F1, 
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ms : -1.f;
 }
+
+// TEX variant: factor rows fetched through the texture path
+// (tex1Dfetch<float4> on a linear-memory texture object) -- does the TEX
+// data path add L1 -> RF bandwidth beside the LSU path?  both = 0: F1 by
+// LDG, F2 by TEX; both = 1: both by TEX.
+template <int U, int BOTH>
+__global__ void __launch_bounds__(256) probe_tex(const uint2 *idx, int64_t n, const float *F1,
+                                                 cudaTextureObject_t T1, cudaTextureObject_t T2,
+                                                 float *sink) {
+  const int lg = threadIdx.x & 7;
+  const int64_t groups = (int64_t)gridDim.x * 32;
+  int64_t g = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t base = g * U; base < n; base += groups * U) {
+    float4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint2 c = idx[min(base + u, n - 1)];
+      if (BOTH) a[u] = tex1Dfetch<float4>(T1, (int)(c.x * 8 + lg));
+      else a[u] = __ldg(reinterpret_cast<const float4 *>(F1 + (uint64_t)c.x * 32 + lg * 4));
+      b[u] = tex1Dfetch<float4>(T2, (int)(c.y * 8 + lg));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc.x += a[u].x * b[u].x;
+      acc.y += a[u].y * b[u].y;
+      acc.z += a[u].z * b[u].z;
+      acc.w += a[u].w * b[u].w;
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) sink[0] = acc.x;
+}
+
+static cudaTextureObject_t tex_of(const float *p, int64_t floats) {
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<float *>(p);
+  rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+  rd.res.linear.sizeInBytes = (size_t)floats * 4;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t t = 0;
+  cudaCreateTextureObject(&t, &rd, &td, nullptr);
+  return t;
+}
+
+extern "C" float gather_probe_tex(const uint2 *idx, int64_t n, const float *F1, int64_t f1_floats,
+                                  const float *F2, int64_t f2_floats, float *sink, int u,
+                                  int blocks, int both) {
+  cudaTextureObject_t T1 = tex_of(F1, f1_floats), T2 = tex_of(F2, f2_floats);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int it = 0; it < 2; ++it) {
+    cudaEventRecord(e0);
+    if (both) {
+      if (u == 4) probe_tex<4, 1><<<blocks, 256>>>(idx, n, F1, T1, T2, sink);
+      else probe_tex<8, 1><<<blocks, 256>>>(idx, n, F1, T1, T2, sink);
+    } else {
+      if (u == 4) probe_tex<4, 0><<<blocks, 256>>>(idx, n, F1, T1, T2, sink);
+      else probe_tex<8, 0><<<blocks, 256>>>(idx, n, F1, T1, T2, sink);
+    }
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaDestroyTextureObject(T1);
+  cudaDestroyTextureObject(T2);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ms : -1.f;
+}

@@ -39,3 +39,16 @@ for u in (4, 8):
         ms = L.gather_probe_tma(idx.data_ptr(), n, fs.factors[1].data_ptr(), fs.factors[2].data_ptr(),
                                 sink.data_ptr(), u, blocks)
         print(f"TMA layout    U={u} blocks={blocks:5d}: {ms:.3f} ms  ({n * 256 / ms / 1e6:.0f} GB/s of rows)")
+
+L.gather_probe_tex.restype = ctypes.c_float
+L.gather_probe_tex.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                               ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int]
+for both in (0, 1):
+    for u in (4, 8):
+        for blocks in (148 * 8, 148 * 32):
+            ms = L.gather_probe_tex(idx.data_ptr(), n, fs.factors[1].data_ptr(), fs.factors[1].numel(),
+                                    fs.factors[2].data_ptr(), fs.factors[2].numel(), sink.data_ptr(),
+                                    u, blocks, both)
+            what = "TEX both" if both else "LDG+TEX"
+            print(f"{what:13s} U={u} blocks={blocks:5d}: {ms:.3f} ms  ({n * 256 / ms / 1e6:.0f} GB/s of rows)")
