@@ -456,6 +456,138 @@ static int orc_big_super_shard(const orc_hash_job_t *J, int64_t s, int T) {
   return rc;
 }
 
+/* Memory-lean variant for Morton keys of <= 32 bits (c2, c5): every element
+ * of the super-shard is one word (key << 32 | input position); the words
+ * enter in position order, so a stable LSD radix sort on the key bits alone
+ * gives the canonical (key, position) order.  16 bytes of scratch per
+ * element instead of 24 (c5's first mode-0 super-shard holds 2.5B). */
+typedef struct {
+  const orc_hash_job_t *J;
+  uint64_t *P, *Q;
+  int64_t lo, n, s;
+  int64_t *hist;                     /* [threads][2048] */
+  pthread_barrier_t *bar;
+  int t, T;
+} orc_pk_t;
+
+static void *orc_pk_run(void *arg) {
+  orc_pk_t *W = (orc_pk_t *)arg;
+  const orc_hash_job_t *J = W->J;
+  const int64_t a = W->n * W->t / W->T, b = W->n * (W->t + 1) / W->T;
+  for (int64_t r = a; r < b; ++r) {
+    const uint32_t id = J->ids[W->lo + r];
+    W->P[r] = orc_morton_row(J, J->coords + (int64_t)id * J->cs) << 32 | id;
+  }
+  uint64_t *pa = W->P, *pb = W->Q;
+  int64_t *h = W->hist + (int64_t)W->t * 2048;
+  for (int sh = 32; sh < 32 + J->total; sh += 11) {
+    pthread_barrier_wait(W->bar);
+    memset(h, 0, sizeof(int64_t) * 2048);
+    for (int64_t r = a; r < b; ++r) h[(pa[r] >> sh) & 2047]++;
+    pthread_barrier_wait(W->bar);
+    if (W->t == 0) {
+      int64_t run = 0;
+      for (int d = 0; d < 2048; ++d)
+        for (int t = 0; t < W->T; ++t) {
+          int64_t *c = W->hist + (int64_t)t * 2048 + d;
+          const int64_t x = *c;
+          *c = run;
+          run += x;
+        }
+    }
+    pthread_barrier_wait(W->bar);
+    for (int64_t r = a; r < b; ++r) pb[h[(pa[r] >> sh) & 2047]++] = pa[r];
+    uint64_t *tp = pa; pa = pb; pb = tp;
+  }
+  pthread_barrier_wait(W->bar);
+  for (int64_t r = a; r < b; ++r) {
+    const int64_t id = (int64_t)(pa[r] & 0xFFFFFFFFull);
+    const int64_t sh = J->first[W->s] + r / J->g;
+    __atomic_fetch_add(&J->hash[sh], orc_elem_hash(J->coords + id * J->cs, J->nmodes,
+                                                    J->vbits[id * J->vs]), __ATOMIC_RELAXED);
+    __atomic_fetch_add(&J->count[sh], 1, __ATOMIC_RELAXED);
+  }
+  return NULL;
+}
+
+static int orc_big_packed(const orc_hash_job_t *J, int64_t s, int T) {
+  const int64_t lo = J->ss_off[s], n = J->ss_off[s + 1] - lo;
+  uint64_t *P = (uint64_t *)malloc((size_t)n * 8), *Q = (uint64_t *)malloc((size_t)n * 8);
+  int64_t *hist = (int64_t *)malloc(sizeof(int64_t) * 2048 * T);
+  pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * T);
+  orc_pk_t *W = (orc_pk_t *)malloc(sizeof(orc_pk_t) * T);
+  int rc = 0;
+  if (!P || !Q || !hist || !tid || !W) {
+    rc = -1;
+  } else {
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)T);
+    for (int t = 0; t < T; ++t) {
+      W[t] = (orc_pk_t){J, P, Q, lo, n, s, hist, &bar, t, T};
+      pthread_create(&tid[t], NULL, orc_pk_run, &W[t]);
+    }
+    for (int t = 0; t < T; ++t) pthread_join(tid[t], NULL);
+    pthread_barrier_destroy(&bar);
+  }
+  free(P); free(Q); free(hist); free(tid); free(W);
+  return rc;
+}
+
+/* Stable counting sort of element ids by super-shard, by all threads:
+ * per-thread counts over contiguous id ranges, thread-ordered offsets,
+ * in-order scatter -- ids ascending inside every super-shard. */
+typedef struct {
+  const int32_t *coords; int64_t cs; int mode; int64_t m;
+  int64_t nnz, K;
+  int64_t *cnt;                      /* [threads][K] counts, then offsets */
+  uint32_t *ids;
+  pthread_barrier_t *bar;
+  int t, T;
+} orc_cs_t;
+
+static void *orc_cs_run(void *arg) {
+  orc_cs_t *C = (orc_cs_t *)arg;
+  const int64_t a = C->nnz * C->t / C->T, b = C->nnz * (C->t + 1) / C->T;
+  int64_t *c = C->cnt + (int64_t)C->t * C->K;
+  for (int64_t i = a; i < b; ++i) c[C->coords[i * C->cs + C->mode] / C->m]++;
+  pthread_barrier_wait(C->bar);
+  if (C->t == 0) {
+    int64_t run = 0;
+    for (int64_t s = 0; s < C->K; ++s)
+      for (int t = 0; t < C->T; ++t) {
+        int64_t *x = C->cnt + (int64_t)t * C->K + s;
+        const int64_t v = *x;
+        *x = run;
+        run += v;
+      }
+  }
+  pthread_barrier_wait(C->bar);
+  for (int64_t i = a; i < b; ++i) C->ids[c[C->coords[i * C->cs + C->mode] / C->m]++] = (uint32_t)i;
+  return NULL;
+}
+
+static int orc_counting_sort(const int32_t *coords, int64_t cs, int mode, int64_t m, int64_t nnz,
+                             int64_t K, int T, uint32_t *ids) {
+  if ((int64_t)T * K > (1ll << 28)) T = 1;   /* per-thread counts must stay small */
+  int64_t *cnt = (int64_t *)calloc((size_t)T * (size_t)K, sizeof(int64_t));
+  pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * T);
+  orc_cs_t *C = (orc_cs_t *)malloc(sizeof(orc_cs_t) * T);
+  if (!cnt || !tid || !C) {
+    free(cnt); free(tid); free(C);
+    return -1;
+  }
+  pthread_barrier_t bar;
+  pthread_barrier_init(&bar, NULL, (unsigned)T);
+  for (int t = 0; t < T; ++t) {
+    C[t] = (orc_cs_t){coords, cs, mode, m, nnz, K, cnt, ids, &bar, t, T};
+    pthread_create(&tid[t], NULL, orc_cs_run, &C[t]);
+  }
+  for (int t = 0; t < T; ++t) pthread_join(tid[t], NULL);
+  pthread_barrier_destroy(&bar);
+  free(cnt); free(tid); free(C);
+  return 0;
+}
+
 int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, int64_t vs,
                      int64_t nnz, int nmodes, int mode, const int64_t *m, const int64_t *k,
                      int64_t g, int threads, int64_t *ss_counts, uint64_t *hash,
@@ -500,7 +632,10 @@ int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, i
     if (ss_counts[s] > big) big = ss_counts[s];
   }
   /* stable counting sort of element ids by super-shard (ids ascending) */
-  for (int64_t i = 0; i < nnz; ++i) ids[fill[coords[i * cs + mode] / m[mode]]++] = (uint32_t)i;
+  if (orc_counting_sort(coords, cs, mode, m[mode], nnz, K, threads, ids) != 0) {
+    free(off); free(first); free(fill); free(queue); free(ids);
+    return -1;
+  }
   {
     int64_t *pairs = (int64_t *)malloc(sizeof(int64_t) * 2 * (K > 0 ? K : 1));
     if (!pairs) {
@@ -521,7 +656,9 @@ int orc_shard_hashes(const int32_t *coords, int64_t cs, const uint32_t *vbits, i
    * heads: c4's first super-shard) are sorted by all threads together */
   int64_t nbig = 0;
   while (threads > 1 && nbig < K && ss_counts[queue[nbig]] * 2 * threads > nnz) {
-    if (orc_big_super_shard(&J, queue[nbig], threads) != 0) {
+    const int rc = J.total <= 32 ? orc_big_packed(&J, queue[nbig], threads)
+                                 : orc_big_super_shard(&J, queue[nbig], threads);
+    if (rc != 0) {
       free(off); free(first); free(fill); free(queue); free(ids);
       return -1;
     }
