@@ -16,9 +16,9 @@ not fit"), through the public API on one B200:
   reference's canonical shard assignment (north_star: "per-shard nonzero
   multisets and offsets"): c2 exactly -- every nonzero's shard and value
   against ``oracle.canonical_build`` at the bench's own parameters, plus the
-  shard offsets; c3 and c4 (and c5 with FLYCOO_C5_DIGESTS=1: ~160 GB of host
-  memory) through per-shard (hash, count) digests against the streaming C
-  restatement ``oracle.shard_hashes`` and the shard offsets against the
+  shard offsets; c3, c4 and c5 (c5: ~110 GB of host memory;
+  FLYCOO_C5_DIGESTS=0 skips it) through per-shard (hash, count) digests
+  against the streaming C restatement ``oracle.shard_hashes`` and the shard offsets against the
   super-shard fills it counts.
 """
 import os
