@@ -60,15 +60,3 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 print(f"copy of records {x.numel()*4/1e9:.2f} GB: {ms:.3f} ms = {2*x.numel()*4/ms/1e6:.0f} GB/s")
-
-# per-phase cycle split (only with the FAST_PHASE_TIMING experimental build)
-import ctypes
-L = _lib.load()
-if hasattr(L, "fc_debug_phase_cycles"):
-    buf = (ctypes.c_ulonglong * 5)()
-    L.fc_debug_phase_cycles(buf, 1)
-    run(0, 1, 1, reps=5)
-    L.fc_debug_phase_cycles(buf, 1)
-    tot = sum(buf)
-    print("phase cycles (thread 0 of each CTA, mode 0 x5): " + ", ".join(
-        f"{n} {100 * v / tot:.1f}%" for n, v in zip(("D(prev)+A", "B1 rank", "B2 scan", "B3 scatter", "C"), buf)))
