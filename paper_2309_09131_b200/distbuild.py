@@ -12,14 +12,18 @@ Steps (P ranks, element e with global input position gid(e)):
 1. plan: per-mode super-shard histograms, all-reduced (layout.py:487-497);
    every rank derives the same PartitionPlan and the same per-mode slice
    bounds of the fused exchange (peer.slice_bounds).
-2. canonical shard ids, per mode n: elements travel to the rank owning their
-   mode-n super-shard (contiguous super-shard ranges balanced by fill); it
-   orders them by (iv_n, Morton, gid) -- lexsort(seq, lo, hi, iv_n),
-   layout.py:484 -- as three stable sorts (they arrive in gid order), cuts
-   g-shards (layout.py:491-492) and returns sid_n(e) to e's home rank.
-3. global positions, per mode n: the same routing, ordered by (sid_n,
-   sid_{n-1}, Morton, gid) -- the B200 order of build_device_sharded --
-   gives pos_n(e) = the owner's first element offset + rank; back home.
+2. canonical shard ids, per mode n: a sample sort of the elements on the
+   canonical order (iv_n, Morton, gid) -- lexsort(seq, lo, hi, iv_n),
+   layout.py:484: elements travel to the rank owning their range of a
+   monotone route key (iv_n, leading Morton bits; splitters from an
+   all-gathered sample, so a Zipf-heavy super-shard -- c5 mode 0 has two --
+   is spread over ranks), which orders them with three stable sorts (they
+   arrive in gid order); position = the rank's global offset (exclusive scan
+   of the received counts) + local rank; g-shards cut as layout.py:491-492;
+   sid_n(e) goes back to e's home rank.
+3. global positions, per mode n: the same sample sort on the B200 order
+   (sid_n, sid_{n-1}, Morton, gid) of build_device_sharded gives pos_n(e);
+   back home.
 4. slices: (pos_n(e), pos_{n+1}(e)) goes to the rank whose mode-n slice holds
    pos_n(e) (its slot map entry), and e's record to the owner of pos_0(e).
 
@@ -94,17 +98,6 @@ class _Exchange:
         return out
 
 
-def _ss_ranges(counts: np.ndarray, world: int) -> np.ndarray:
-    """world + 1 contiguous super-shard bounds balanced by fill."""
-    c = np.concatenate(([0], np.cumsum(counts)))
-    total = c[-1]
-    b = [0]
-    for p in range(1, world):
-        b.append(max(b[-1], int(np.searchsorted(c, p * total / world, side="left"))))
-    b.append(len(counts))
-    return np.minimum(np.asarray(b, dtype=np.int64), len(counts))
-
-
 def _stable_sort_by(perm: torch.Tensor, key: torch.Tensor) -> torch.Tensor:
     """perm reordered stably by key[perm]."""
     return perm[torch.argsort(key[perm], stable=True)]
@@ -124,6 +117,7 @@ class LocalLayout:
         self.slots = slots            # per mode: int32 (uint32 bits) global next-mode positions
         self.device = torch.device(device)
         self.num_modes = plan.num_modes
+        self.received = []            # elements this rank sorted in each sample-sort step
 
     def records_slice(self, lo: int, hi: int):
         b = self.bounds[0]
@@ -171,19 +165,56 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
     plan = plan_from_counts(params, counts)
     bounds = slice_bounds(plan, world, R, dev)
 
-    # routing by super-shard owner, shared by steps 2 and 3
-    exch, ss_bounds = [], []
-    for n in range(N):
-        sb = _ss_ranges(counts[n], world)
-        ss_bounds.append(sb)
-        dest = torch.searchsorted(torch.as_tensor(sb[1:-1], device=dev), iv[:, n].contiguous(),
-                                  right=True)
-        exch.append(_Exchange(dest, world, group, host))
+    W = sum(int(x - 1).bit_length() if x > 1 else 0 for x in k)
+    received = []
+    nsh = [plan.total_shards(n) for n in range(N)]
+    sbits = [max(x - 1, 1).bit_length() for x in nsh]
+
+    def route_key(fields):
+        """Monotone 63-bit summary of a lexicographic key given as (values,
+        bits) fields, most significant first: the fields are packed from the
+        top and the last one (the Morton key) is truncated to what is left --
+        equal full keys give equal route keys, smaller full keys never give
+        larger ones."""
+        key = torch.zeros(n_loc, dtype=torch.int64, device=dev)
+        left = 63
+        for vals_, bits in fields:
+            take = min(bits, left)
+            if take <= 0:
+                break
+            key = (key << take) | (vals_ >> (bits - take))
+            left -= take
+        return key << left if left > 0 else key
+
+    def sample_sort(rkey):
+        """Exchange routing elements to the owner of their route-key range
+        (splitters from an all-gathered sample of 1024 keys per rank) and the
+        global position of the first element each rank receives."""
+        ns = 1024
+        if n_loc:
+            idx = torch.linspace(0, n_loc - 1, ns, device=dev).round().to(torch.int64)
+            smp = torch.sort(rkey)[0][idx]
+        else:
+            smp = torch.full((ns,), (1 << 63) - 1, dtype=torch.int64, device=dev)
+        allsmp = [torch.empty_like(smp.cpu() if host else smp) for _ in range(world)]
+        dist.all_gather(allsmp, smp.cpu() if host else smp, group=group)
+        pool = torch.sort(torch.cat([t.to(dev) for t in allsmp]))[0]
+        spl = pool[[(p * pool.numel()) // world for p in range(1, world)]]
+        dest = torch.searchsorted(spl, rkey, right=True)
+        E = _Exchange(dest, world, group, host)
+        received.append(sum(E.recv_l))
+        got = torch.tensor(E.recv_l, dtype=torch.int64)
+        counts_all = [torch.empty_like(got) for _ in range(world)]
+        dist.all_gather(counts_all, got if host else got.to(dev), group=group)
+        per_rank = torch.stack([t.cpu() for t in counts_all]).sum(1)
+        base = int(per_rank[:rank].sum())
+        return E, base
 
     # 2. canonical shard ids (layout.py:484-492)
     sid = []
     for n in range(N):
-        E = exch[n]
+        ivb = max(k[n] - 1, 1).bit_length()
+        E, base = sample_sort(route_key([(iv[:, n], ivb), (mkey, max(W, 1))]))
         r_gid = E.forward(gid)
         r_key = E.forward(mkey)
         r_iv = E.forward(iv[:, n].contiguous())
@@ -193,7 +224,6 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
         offs = torch.as_tensor(plan.ss_elem_offsets[n], device=dev)
         first = torch.as_tensor(plan.ss_first_shard[n], device=dev)
         s_iv = r_iv[order]
-        base = int(plan.ss_elem_offsets[n][ss_bounds[n][rank]])
         pos = base + torch.arange(order.shape[0], device=dev, dtype=torch.int64)
         sid_sorted = first[s_iv] + (pos - offs[s_iv]) // g
         r_sid = torch.empty_like(sid_sorted)
@@ -203,8 +233,9 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
     # 3. global positions in the B200 order (sid_n, sid_{n-1}, Morton, gid)
     gpos = []
     for n in range(N):
-        E = exch[n]
         prev = (n - 1) % N
+        E, base = sample_sort(route_key([(sid[n], sbits[n]), (sid[prev], sbits[prev]),
+                                         (mkey, max(W, 1))]))
         r_gid = E.forward(gid)
         r_key = E.forward(mkey)
         r_sn = E.forward(sid[n])
@@ -213,7 +244,6 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
         order = _stable_sort_by(order, r_key)
         order = _stable_sort_by(order, r_sp)
         order = _stable_sort_by(order, r_sn)
-        base = int(plan.ss_elem_offsets[n][ss_bounds[n][rank]])
         r_pos = torch.empty(order.shape[0], dtype=torch.int64, device=dev)
         r_pos[order] = base + torch.arange(order.shape[0], device=dev, dtype=torch.int64)
         gpos.append(E.backward(r_pos))
@@ -251,4 +281,6 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
         r_val = E.forward(v)
         val = torch.empty(n0, dtype=torch.float32, device=dev)
         val[r_at] = r_val
-    return LocalLayout(plan, bounds, rank, crd, val, slots, dev)
+    out = LocalLayout(plan, bounds, rank, crd, val, slots, dev)
+    out.received = received
+    return out
