@@ -98,6 +98,12 @@ class _Exchange:
         return out
 
 
+def _sample_index(n: int, ns: int, device) -> torch.Tensor:
+    """ns evenly spaced indices into [0, n), in exact integer arithmetic (a
+    float linspace rounds past n - 1 once n exceeds 2^24)."""
+    return (torch.arange(ns, dtype=torch.int64, device=device) * (n - 1)) // max(ns - 1, 1)
+
+
 def _stable_sort_by(perm: torch.Tensor, key: torch.Tensor) -> torch.Tensor:
     """perm reordered stably by key[perm]."""
     return perm[torch.argsort(key[perm], stable=True)]
@@ -192,8 +198,7 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
         global position of the first element each rank receives."""
         ns = 1024
         if n_loc:
-            idx = torch.linspace(0, n_loc - 1, ns, device=dev).round().to(torch.int64)
-            smp = torch.sort(rkey)[0][idx]
+            smp = torch.sort(rkey)[0][_sample_index(n_loc, ns, dev)]
         else:
             smp = torch.full((ns,), (1 << 63) - 1, dtype=torch.int64, device=dev)
         allsmp = [torch.empty_like(smp.cpu() if host else smp) for _ in range(world)]

@@ -100,3 +100,14 @@ def test_morton_key_matches_oracle():
     assert not hi.any()
     got = morton_key(torch.from_numpy(iv), k).numpy().view(np.uint64)
     assert np.array_equal(got, lo)
+
+
+def test_sample_index_stays_in_range():
+    """Sample positions for the splitters at the bench's block sizes (c2 at
+    2 ranks: 38.45M elements per rank; c5 at 8: 450M): float linspace would
+    round the last index to n."""
+    from paper_2309_09131_b200.distbuild import _sample_index
+    for n in (1, 2, 1023, 1024, 38_450_000, 450_000_000, 3_600_000_000):
+        idx = _sample_index(n, 1024, "cpu")
+        assert int(idx.min()) == 0 and int(idx.max()) == n - 1
+        assert bool((idx[1:] >= idx[:-1]).all())
