@@ -445,32 +445,34 @@ def run_ours(args, rank, world, local):
             return graph.run(None if fs is factors else fs).factors
         if peer_graph is not None and not eager:
             return peer_graph.run(list(flist))
+        def timed(fn, n):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn(n)
+            e1.record()
+            if mode_secs is not None:
+                e1.synchronize()
+                mode_secs.append(e0.elapsed_time(e1) / 1e3)
+            return out
+
         if dt is not None and exchange == "p2p":
             if updated:
                 return peer_sweep_all_modes(dt, list(flist), mode_seconds=mode_secs)
-            outs = [peer_mttkrp_mode(dt, list(flist), n).clone() for n in range(N)]
+            outs = [timed(lambda n: peer_mttkrp_mode(dt, list(flist), n).clone(), n)
+                    for n in range(N)]
             dt.check()
             return outs
         if dt is not None:
             if updated:
                 return dist_sweep_all_modes(dt, list(flist), ops, mode_seconds=mode_secs)
-            outs = [dist_mttkrp_mode(dt, list(flist), n, ops) for n in range(N)]
+            outs = [timed(lambda n: dist_mttkrp_mode(dt, list(flist), n, ops), n) for n in range(N)]
             ops.check(dt)
             return outs
         if updated:
             return sweep_all_modes(st, fs, smap, mode_seconds=mode_secs).factors
         from paper_2309_09131_b200 import mttkrp_mode
-        outs = []
-        for n in range(N):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            outs.append(mttkrp_mode(st, fs, n, smap))
-            e1.record()
-            if mode_secs is not None:
-                e1.synchronize()
-                mode_secs.append(e0.elapsed_time(e1) / 1e3)
-        return outs
+        return [timed(lambda n: mttkrp_mode(st, fs, n, smap), n) for n in range(N)]
 
     for _ in range(max(args.warmup, 0)):
         step(factors)
@@ -520,7 +522,7 @@ def run_ours(args, rank, world, local):
     # multi-GPU: a rank's share of the compulsory bytes over its mode time
     # (which then also contains the exchange and the all-gather)
     per_mode = compulsory_bytes(nnz, dims, R)
-    kern_s = sum(mode_secs)
+    kern_s = sum(mode_secs) or t_ms / 1e3
     basis = "CUDA events around each eager mode pass (K1 + K2)"
     if graph is not None or peer_graph is not None:
         # graph replay: the timed sweeps contain only the passes (K1 + K2), with
