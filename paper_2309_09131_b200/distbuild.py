@@ -159,11 +159,15 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
     iv = torch.stack([c[:, w] // m[w] for w in range(N)], 1)
     mkey = morton_key(iv, k)
 
+    def coll(t: torch.Tensor) -> torch.Tensor:
+        """A tensor where this group's backend takes it: host for gloo, the
+        device for NCCL."""
+        return t.cpu() if host else t.to(dev)
+
     # 1. plan from all-reduced histograms (layout.py:487-497)
     counts = []
     for n in range(N):
-        h = torch.bincount(iv[:, n], minlength=k[n]).to(torch.int64)
-        hh = h.cpu() if host else h
+        hh = coll(torch.bincount(iv[:, n], minlength=k[n]).to(torch.int64))
         dist.all_reduce(hh, group=group)
         counts.append(hh.cpu().numpy())
     if int(sum(x.sum() for x in counts)) != N * params.nnz:
@@ -201,16 +205,17 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
             smp = torch.sort(rkey)[0][_sample_index(n_loc, ns, dev)]
         else:
             smp = torch.full((ns,), (1 << 63) - 1, dtype=torch.int64, device=dev)
-        allsmp = [torch.empty_like(smp.cpu() if host else smp) for _ in range(world)]
-        dist.all_gather(allsmp, smp.cpu() if host else smp, group=group)
+        smp = coll(smp)
+        allsmp = [torch.empty_like(smp) for _ in range(world)]
+        dist.all_gather(allsmp, smp, group=group)
         pool = torch.sort(torch.cat([t.to(dev) for t in allsmp]))[0]
         spl = pool[[(p * pool.numel()) // world for p in range(1, world)]]
         dest = torch.searchsorted(spl, rkey, right=True)
         E = _Exchange(dest, world, group, host)
         received.append(sum(E.recv_l))
-        got = torch.tensor(E.recv_l, dtype=torch.int64)
+        got = coll(torch.tensor(E.recv_l, dtype=torch.int64))
         counts_all = [torch.empty_like(got) for _ in range(world)]
-        dist.all_gather(counts_all, got if host else got.to(dev), group=group)
+        dist.all_gather(counts_all, got, group=group)
         per_rank = torch.stack([t.cpu() for t in counts_all]).sum(1)
         base = int(per_rank[:rank].sum())
         return E, base

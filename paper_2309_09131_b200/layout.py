@@ -477,6 +477,9 @@ def _mix64(x: torch.Tensor) -> torch.Tensor:
     return x ^ ((x >> 31) & ((1 << 33) - 1))
 
 
+_BUCKET_KEYS = 1 << 28  # keys per sort bucket of the duplicate check
+
+
 def device_has_duplicates(coords: torch.Tensor, dims, buckets: int | None = None) -> bool:
     """True iff two rows of the (nnz, N) integer coordinate tensor are equal
     -- the reference's "duplicate coordinates" check (coo.py:88-89), run
@@ -497,8 +500,10 @@ def device_has_duplicates(coords: torch.Tensor, dims, buckets: int | None = None
         else:
             salt = (((n + 1) * _MIX1 + (1 << 63)) % (1 << 64)) - (1 << 63)  # wrapped to int64
             key = _mix64(key ^ _mix64(c + salt))
-    if buckets is None:
-        buckets = max(1, min(16, -(-nnz // (1 << 28))))
+    if buckets is None:  # a power of two, <= _BUCKET_KEYS keys per bucket on average, <= 16
+        buckets = 1
+        while buckets < 16 and nnz > buckets * _BUCKET_KEYS:
+            buckets *= 2
     bsel = _mix64(key) & (buckets - 1) if buckets > 1 and (buckets & (buckets - 1)) == 0 else None
     if buckets > 1 and bsel is None:
         raise ValueError("buckets must be a power of two")

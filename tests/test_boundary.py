@@ -80,3 +80,13 @@ def test_device_duplicate_check_hash_collisions():
     rows = np.array([[1, 2], [2, 1], [3, 4]], dtype=np.int64)
     assert not device_has_duplicates(torch.as_tensor(rows), dims)
     assert device_has_duplicates(torch.as_tensor(np.concatenate([rows, rows[:1]])), dims)
+
+
+def test_device_duplicate_check_bucket_count(monkeypatch):
+    """The automatic bucket count is a power of two for any size (1.74B
+    nonzeros asked for 7 buckets before and raised)."""
+    import paper_2309_09131_b200.layout as L
+    rows = torch.as_tensor(np.stack([np.arange(1000), np.arange(1000)], 1))
+    monkeypatch.setattr(L, "_BUCKET_KEYS", 300)  # tiny buckets: 4 for 1000 keys
+    assert not L.device_has_duplicates(rows, (1000, 1000))
+    assert L.device_has_duplicates(torch.cat([rows, rows[:1]]), (1000, 1000))
