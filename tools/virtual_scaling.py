@@ -86,7 +86,7 @@ def main():
         del ranks
         torch.cuda.empty_cache()
     tag = f"c{cfg}" if nnz is None else f"c{cfg}_nnz{nnz}"
-    out = Path(__file__).resolve().parents[1] / "profiles" / f"r1_virtual_scaling_{tag}.json"
+    out = Path(__file__).resolve().parents[1] / "profiles" / f"r2_virtual_scaling_{tag}.json"
     out.write_text(json.dumps(result, indent=1))
 
 
