@@ -628,6 +628,8 @@ def run_ours(args, rank, world, local):
                                  "lean (bucketed generator, layout.build_device_sharded_lean)"
                                  if lean else "regular"),
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
+                       # SURVEY 8(d) also asks for nnz / t_sweep (value is N * nnz / t_sweep)
+                       "nnz_per_s_sweep": nnz / (ms_per_step / 1e3),
                        # median over the measured sweeps of each mode pass
                        "mode_ms": [round(1e3 * statistics.median(mode_secs[n::N]), 4)
                                    for n in range(N)] if mode_secs else []},
