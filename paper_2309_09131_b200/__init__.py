@@ -8,7 +8,8 @@ CUDA kernels (libflycoo.so, C ABI in include/flycoo.h).
 
 from .engine import (REMAP_STRATEGIES, BufferOrderError, RemapCursors, ShardOverflowError,
                      TrafficCounters, mttkrp_mode, remap_store, sweep_all_modes)
-from .coo import CooTensor, Element
+from .coo import CooTensor, Element, parse_frostt, read_frostt, synth_tensor, write_frostt
+from .io import FrosttParseError, load_factor_set, save_factor_set
 from .factors import DeviceFactorSet
 from .layout import (CheckResult, DeviceShardedTensor, PartitionPlan, PlanReport,
                      build_device_sharded, build_sharded, device_has_duplicates, plan_from_counts,

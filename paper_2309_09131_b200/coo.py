@@ -22,7 +22,8 @@ from typing import Sequence
 
 import numpy as np
 
-__all__ = ["CooTensor", "Element", "coords_key", "has_duplicates"]
+__all__ = ["CooTensor", "Element", "coords_key", "has_duplicates", "parse_frostt", "read_frostt",
+           "write_frostt", "synth_tensor"]
 
 
 @dataclass(frozen=True)
@@ -126,3 +127,35 @@ class CooTensor:
         if rtol == 0.0:
             return bool(np.array_equal(va, vb))
         return bool(np.allclose(va, vb, rtol=rtol, atol=0.0))
+
+
+# ------------------------------------------------ reference-shaped entry points
+# The reference's coo module returns and takes CooTensor objects
+# (coo.py:212-355); the array-level implementations live in io.py / synth.py.
+
+def parse_frostt(source, dims=None) -> CooTensor:
+    """FROSTT text (1-based, '#' comments, duplicates summed) -> CooTensor
+    (coo.py:212-272; errors are io.FrosttParseError with the line number)."""
+    from . import io as _io
+    subs, vals, d = _io.parse_frostt(source, dims=dims)
+    return CooTensor(d, subs, vals)
+
+
+def read_frostt(path, dims=None) -> CooTensor:
+    """coo.py:298-299."""
+    from pathlib import Path
+    return parse_frostt(Path(path), dims=dims)
+
+
+def write_frostt(tensor: CooTensor, destination=None):
+    """1-based indices, exact %.17g values; text when `destination` is None
+    (coo.py:302-316)."""
+    from . import io as _io
+    return _io.write_frostt(tensor.subs, tensor.vals, destination)
+
+
+def synth_tensor(dims, nnz: int, seed: int, skew: float = 0.0) -> CooTensor:
+    """The reference's seeded generator (coo.py:323-355), bit-identical."""
+    from . import synth as _synth
+    subs, vals = _synth.synth_tensor(dims, nnz, seed, skew=skew)
+    return CooTensor(tuple(int(d) for d in dims), subs, vals)
