@@ -145,7 +145,13 @@ def build_partitioned(subs: torch.Tensor, vals: torch.Tensor, gid0: int, params:
     from .peer import slice_bounds
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    dev = torch.device(device) if device is not None else subs.device
+    if device is not None:
+        dev = torch.device(device)
+    elif isinstance(subs, torch.Tensor):
+        dev = subs.device
+    else:  # host arrays: the current GPU (CPU when there is none, e.g. gloo tests)
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+            else torch.device("cpu")
     host = dist.get_backend(group) == "gloo"
     N = len(params.dims)
     R = int(R if R is not None else params.rank)
