@@ -72,52 +72,92 @@ def peaks():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every ~2 ms from a thread (a 20-step c2 run lasts ~75 ms, shorter
+    than nvidia-smi's sampling period); nvidia-smi -lms 50 when NVML is not
+    available."""
 
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = None
+        self.rows = []
+        self.proc = self.thread = self.path = None
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.bits = (pynvml.nvmlClocksEventReasonHwSlowdown,
+                         pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwPowerCap)
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            import threading
+            self.stop_flag = threading.Event()
+
+            def poll():
+                p = self.nvml
+                while not self.stop_flag.is_set():
+                    try:
+                        mhz = p.nvmlDeviceGetClockInfo(self.handle, p.NVML_CLOCK_SM)
+                        r = p.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                        self.rows.append((float(mhz), float(self.max_mhz),
+                                          [("Active" if r & b else "Not Active") for b in self.bits]))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (FileNotFoundError, OSError):
             self.proc = None
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        rows = []
-        for line in Path(self.path).read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
+        source = "nvml"
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join()
+        elif self.proc is not None:
+            source = "nvidia-smi"
+            self.proc.terminate()
             try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
-            except ValueError:
-                continue
-        os.unlink(self.path)
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            for line in Path(self.path).read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    self.rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                except ValueError:
+                    continue
+            os.unlink(self.path)
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"]}
+        rows = self.rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        reasons = sorted({self.NAMES[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": source}
 
 
 # -------------------------------------------------------------- workloads
@@ -480,8 +520,6 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     mode_secs = []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -490,6 +528,7 @@ def run_ours(args, rank, world, local):
     resident_bytes = nnz * (4 * N + 4 + 4 * N)
     flush_l2 = resident_bytes < (256 << 20)
     torch.cuda.synchronize()
+    clocks.start()  # sampled from here to the end of the timed steps
     if flush_l2:
         scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         t_ms = 0.0
