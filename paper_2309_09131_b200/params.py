@@ -270,10 +270,11 @@ def device_params(dims: Sequence[int], nnz: int, rank: int, acc_tile_bytes: int 
     if m is None:
         if acc_tile_bytes is None and len(dims) == 3:
             # 3-mode tensors run the packed kernel, whose <= 32-row ranking
-            # (row-owner lanes) wins everywhere measured: c1, c2, c4 (109.5 vs
-            # 115.8 ms at 8 KB), c5
+            # (row-owner lanes) wins everywhere measured: c2, c4 (109.5 vs
+            # 115.8 ms at 8 KB), c5; and c1 (R = 16): 0.121 ms per sweep at 32
+            # rows vs 0.131 at the 4 KB tile's 64 (tools/c1_sweep.sh)
             small = max(1, 4096 // (4 * int(rank)))
-            m = tuple(min(d, small) for d in dims)
+            m = tuple(min(d, small, 32) for d in dims)
         elif acc_tile_bytes is None:
             m = tuple(_auto_rows(d, nnz, rank) for d in dims)
         else:
