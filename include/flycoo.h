@@ -113,6 +113,45 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
                    int do_compute, int do_remap, int acc_in_smem,
                    int32_t *flags, unsigned long long *counters, void *stream);
 
+/* Tile plan.  The layout is static, so every 2048-element tile of a mode's
+ * buffer is sorted by output row the same way in every sweep (the stable
+ * counting sort in front of the row-segmented reduction; the reference's
+ * per-element loop _kernels.py:58-72 has no such step).  fc_tile_plan_emit
+ * runs that ranking once over the buffer that is active for `mode` and
+ * writes, per element, its position in the sorted tile (tile_perm: 2048
+ * uint16 per tile key, the 8 elements of a thread adjacent) and, per tile,
+ * the bin starts (tile_bins, hist_rows uint16 per tile key;
+ * fc_tile_plan_keys(nnz, nchunks) keys; hist_rows = the work plan's, or
+ * m_mode when chunk_rows is NULL).  fc_mode_worker_planned is
+ * fc_mode_worker (do_compute = 1, shared-memory accumulation) reading that
+ * plan instead of ranking: same sorted order, hence bitwise the same sums.
+ * Both return FC_ERR_UNSUPPORTED outside the kernels that take a plan
+ * (3-mode tensors at R = 32, one GPU); callers then use fc_mode_worker.
+ * The plan is valid for the work plan (chunk arrays) it was emitted with and
+ * for the canonical (slot-remapped) order only. */
+int fc_tile_plan_emit(const void *src_crd, const float *src_val,
+                      const float *const *factors, const int64_t *dims,
+                      int nmodes, int mode, int rank, int64_t out_rows, int64_t m_mode,
+                      const int64_t *chunk_start, const int32_t *chunk_ss,
+                      const int32_t *chunk_part, const int32_t *chunk_rows,
+                      int64_t tile_rows, int64_t hist_rows, int64_t nchunks, int64_t nnz,
+                      int32_t *flags, unsigned long long *counters,
+                      uint16_t *tile_perm, uint16_t *tile_bins, void *stream);
+int64_t fc_tile_plan_keys(int64_t nnz, int64_t nchunks);
+int fc_mode_worker_planned(const void *src_crd, const float *src_val,
+                           void *dst_crd, float *dst_val,
+                           const float *const *factors, const int64_t *dims,
+                           float *out, int nmodes, int mode, int rank,
+                           int64_t out_rows, int64_t m_mode,
+                           const int64_t *chunk_start, const int32_t *chunk_ss,
+                           const int32_t *chunk_part, const int32_t *chunk_rows,
+                           int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                           const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
+                           float *part_ws, float *part_ws2, const uint32_t *dest_slots,
+                           int64_t nnz, int do_remap, int32_t *flags,
+                           unsigned long long *counters, const uint16_t *tile_perm,
+                           const uint16_t *tile_bins, void *stream);
+
 /* Multi-GPU mode pass with the remap fused with the exchange (dist.py,
  * exchange "p2p"): same work plan and arguments as fc_mode_worker, but
  * dest_slots hold GLOBAL mode-(n+1) positions and every record is stored

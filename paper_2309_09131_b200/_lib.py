@@ -57,6 +57,23 @@ _SIGS = {
         _vp, _vp,                      # peer_part_ws (host array), chunk_owner (device int32)
         _vp]),                         # stream
     "fc_reduce_partials": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
+    "fc_tile_plan_emit": (_int, [
+        _vp, _vp, _vp, _vp,            # src_crd, src_val, factors, dims
+        _int, _int, _int, _i64, _i64,  # nmodes, mode, rank, out_rows, m_mode
+        _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks
+        _i64, _vp, _vp,                # nnz, flags, counters
+        _vp, _vp, _vp]),               # tile_perm, tile_bins, stream
+    "fc_tile_plan_keys": (_i64, [_i64, _i64]),
+    "fc_mode_worker_planned": (_int, [
+        _vp, _vp, _vp, _vp,            # src_crd, src_val, dst_crd, dst_val
+        _vp, _vp, _vp,                 # factors, dims, out
+        _int, _int, _int,              # nmodes, mode, rank
+        _i64, _i64,                    # out_rows, m_mode
+        _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks
+        _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
+        _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots, nnz
+        _int, _vp, _vp,                # do_remap, flags, counters
+        _vp, _vp, _vp]),               # tile_perm, tile_bins, stream
     "fc_ipc_handle_bytes": (_int, []),
     "fc_ipc_alloc": (_int, [_i64, _vp]),
     "fc_ipc_free": (_int, [_vp]),
@@ -95,6 +112,8 @@ _SIGS = {
     "fc_synth_mark_first": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fc_synth_uniform": (_int, [_c.c_uint64, _c.c_uint32, _i64, _vp, _int, _vp]),
 }
+
+ERR_UNSUPPORTED = -2  # FC_ERR_UNSUPPORTED (flycoo.h)
 
 _lib = None
 _lock = threading.Lock()

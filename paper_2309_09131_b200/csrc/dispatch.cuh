@@ -13,10 +13,24 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   if constexpr (NM == 3) {
     // 8-byte sorted records when the two input coordinates fit 32 bits
     const KernelVariant &kv = kernel_variant();
+    if (a.plan) {
+      // tile plan: the R = 32 packed kernels of one GPU (tile keys: t0 / kTile + chunk)
+      static_assert(kFTile == kTile, "the tile plan is indexed by 2048-element tiles");
+      if constexpr (RT == 32 && !PEER) {
+        if (a.pack_shift > 0 && kv.pack)
+          return a.plan == 1 ? launch_pack<MODE, LPG, RT, false, false, 1>(a, nchunks, st)
+                             : launch_pack<MODE, LPG, RT, false, false, 2>(a, nchunks, st);
+        if (a.pack_shift == 0 && kv.pack_wide)
+          return a.plan == 1 ? launch_pack<MODE, LPG, RT, false, true, 1>(a, nchunks, st)
+                             : launch_pack<MODE, LPG, RT, false, true, 2>(a, nchunks, st);
+      }
+      return FC_ERR_UNSUPPORTED;
+    }
     if (a.pack_shift > 0 && kv.pack) return launch_pack<MODE, LPG, RT, PEER>(a, nchunks, st);
     // wider coordinates: {c_w1, c_w2} + value array, rows from the bins
     if (a.pack_shift == 0 && kv.pack_wide) return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
+  if (a.plan) return FC_ERR_UNSUPPORTED;
   return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
 }
 

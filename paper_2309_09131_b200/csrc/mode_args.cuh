@@ -58,6 +58,15 @@ struct ModeArgs {
   // super-shard whose chunks span GPUs gets its partial tiles written into
   // the owner's workspace, which reduces them after a barrier.
   const int32_t *chunk_owner;
+  // Tile plan (static layout => static per-tile sort): plan = 1 reads every
+  // element's position in its row-sorted tile (plan_perm: 2048 uint16 per tile
+  // key t0 / tile + chunk, thread-major -- element j * 256 + tid at tid * 8 + j)
+  // and every tile's bin starts (plan_bins, hist_rows uint16 per tile key)
+  // instead of ranking the tile; plan = 2 ranks as usual and
+  // writes them (no compute, no remap).
+  uint16_t *plan_perm;
+  uint16_t *plan_bins;
+  int plan;
 };
 
 // Checked build (make CHECKED=1 -> libflycoo_checked.so, FC_DEVICE_CHECKS):
@@ -174,6 +183,11 @@ __device__ __forceinline__ int4 ld_stream_v4(const int4 *p) {
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
   uint32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u16(const uint16_t *p) {
+  uint16_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float ld_stream_f32(const float *p) {

@@ -519,7 +519,8 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
                             const uint32_t *dest_slots, int64_t nnz, int do_compute,
                             int do_remap, int acc_in_smem, int32_t *flags,
                             unsigned long long *counters, void *stream, const PeerTable &peers,
-                            const int32_t *chunk_owner = nullptr) {
+                            const int32_t *chunk_owner = nullptr, uint16_t *plan_perm = nullptr,
+                            uint16_t *plan_bins = nullptr, int plan = 0) {
   FC_CHECK_ARG(nmodes >= 2 && nmodes <= 8, "nmodes %d outside [2, 8]", nmodes);
   FC_CHECK_ARG(mode >= 0 && mode < nmodes, "mode %d out of range", mode);
   FC_CHECK_ARG(src_crd && flags && counters, "null buffer");
@@ -601,8 +602,16 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
   a.counters = counters;
   a.peers = peers;
   a.chunk_owner = chunk_owner;
+  a.plan_perm = plan_perm;
+  a.plan_bins = plan_bins;
+  a.plan = plan;
+  if (plan) {
+    FC_CHECK_ARG(plan_perm && plan_bins, "null tile plan");
+    if (!acc_in_smem || !fast_ok(a, true) || peers.n > 0) return FC_ERR_UNSUPPORTED;
+  }
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
+  if (plan == 2) return FC_OK;  // plan emission: no sums to reduce
   if (acc_in_smem && nred1 > 0) {
     FC_CHECK_ARG(red1 && part_ws, "null reduce plan");
     const int64_t cells = m_mode * rank;
@@ -637,6 +646,45 @@ int fc_mode_worker(const void *src_crd, const float *src_val, void *dst_crd, flo
                           part_ws2, dest_slots, nnz, do_compute, do_remap, acc_in_smem, flags,
                           counters, stream, none);
 }
+
+int fc_mode_worker_planned(const void *src_crd, const float *src_val, void *dst_crd, float *dst_val,
+                           const float *const *factors, const int64_t *dims, float *out,
+                           int nmodes, int mode, int rank, int64_t out_rows, int64_t m_mode,
+                           const int64_t *chunk_start, const int32_t *chunk_ss,
+                           const int32_t *chunk_part, const int32_t *chunk_rows,
+                           int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                           const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,
+                           float *part_ws, float *part_ws2, const uint32_t *dest_slots,
+                           int64_t nnz, int do_remap, int32_t *flags,
+                           unsigned long long *counters, const uint16_t *tile_perm,
+                           const uint16_t *tile_bins, void *stream) {
+  PeerTable none{};
+  return mode_worker_impl(src_crd, src_val, dst_crd, dst_val, factors, dims, out, nmodes, mode,
+                          rank, out_rows, m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows,
+                          tile_rows, hist_rows, nchunks, red1, nred1, red2, nred2, part_ws,
+                          part_ws2, dest_slots, nnz, 1, do_remap, 1, flags, counters, stream, none,
+                          nullptr, const_cast<uint16_t *>(tile_perm),
+                          const_cast<uint16_t *>(tile_bins), 1);
+}
+
+int fc_tile_plan_emit(const void *src_crd, const float *src_val, const float *const *factors,
+                      const int64_t *dims, int nmodes, int mode, int rank, int64_t out_rows,
+                      int64_t m_mode, const int64_t *chunk_start, const int32_t *chunk_ss,
+                      const int32_t *chunk_part, const int32_t *chunk_rows, int64_t tile_rows,
+                      int64_t hist_rows, int64_t nchunks, int64_t nnz, int32_t *flags,
+                      unsigned long long *counters, uint16_t *tile_perm, uint16_t *tile_bins,
+                      void *stream) {
+  PeerTable none{};
+  // `out` is never written by the emission pass; any non-null pointer passes the checks
+  return mode_worker_impl(src_crd, src_val, nullptr, nullptr, factors, dims,
+                          reinterpret_cast<float *>(tile_perm), nmodes, mode, rank, out_rows,
+                          m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows, tile_rows,
+                          hist_rows, nchunks, nullptr, 0, nullptr, 0, nullptr, nullptr, nullptr,
+                          nnz, 1, 0, 1, flags, counters, stream, none, nullptr, tile_perm,
+                          tile_bins, 2);
+}
+
+int64_t fc_tile_plan_keys(int64_t nnz, int64_t nchunks) { return nnz / kTile + nchunks + 2; }
 
 int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float *const *factors,
                          const int64_t *dims, float *out, int nmodes, int mode, int rank,

@@ -45,7 +45,12 @@ struct PackPlan {
   }
 };
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
+// PLAN: 0 = rank every tile in the kernel; 1 = the tile plan gives every
+// element's sorted position and every tile's bin starts (no ballots, no
+// histogram, no scan: two barriers per tile instead of four); 2 = rank as
+// PLAN 0 and write the plan (nothing else).  The plan is static because the
+// layout is: the same tiles are sorted the same way in every sweep.
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, int PLAN = 0>
 __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kernel(const __grid_constant__ ModeArgs a) {
   using PP = PackPlan<LPG, WIDE>;
   constexpr int G = PP::G;
@@ -86,7 +91,9 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   const int irow0 = (int)row0;
   const bool direct = part == kPartDirect;
   float *out_rows = a.out + row0 * R;
-  if (direct) {
+  if (PLAN == 2) {
+    if (start == end) return;
+  } else if (direct) {
     if (start == end) {
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int i = tid; i < rows * R / 4; i += kFBlock) reinterpret_cast<float4 *>(out_rows)[i] = z;
@@ -113,6 +120,15 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     // ---------------------------------------------------------------- A
     int4 rec[kFIPT];
     uint32_t slot[kFIPT];
+    // tile plan: this tile's key, and the thread's 8 sorted positions as one
+    // 16-byte word (uint16 each, stored thread-major per tile key)
+    const int64_t tkey = t0 / kFTile + chunk;
+    static_assert(PLAN == 0 || kFIPT == 8, "the tile plan packs 8 positions per thread");
+    uint32_t pw[PLAN != 0 ? 4 : 1] = {};
+    if constexpr (PLAN == 1) {
+      const int4 w4 = ld_stream_v4(reinterpret_cast<const int4 *>(a.plan_perm + tkey * kFTile) + tid);
+      pw[0] = (uint32_t)w4.x, pw[1] = (uint32_t)w4.y, pw[2] = (uint32_t)w4.z, pw[3] = (uint32_t)w4.w;
+    }
     if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -134,7 +150,9 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         }
       }
     }
-    for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
+    if constexpr (PLAN != 1) {
+      for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
+    }
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int e = j * kFBlock + tid;
@@ -144,12 +162,44 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         }
       }
     }
-    {  // a record outside the chunk's super-shard rows (invalid items: -1 by design)
+    if constexpr (PLAN != 1) {  // a record outside the chunk's super-shard rows (invalid items: -1 by design)
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) bad |= (j * kFBlock + tid < cnt) && key_of(rec[j]) < 0;
       if (bad) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
     }
+    if constexpr (PLAN == 1) {
+      // ------------------------------------------------------------ B (planned)
+      // bin starts and the pieces' first bins from the tile plan, records
+      // straight to their sorted positions
+      if (tid < rows) {
+        const uint16_t *tb = a.plan_bins + tkey * a.hist_rows;
+        const int bstart = tb[tid];
+        const int tot = (tid + 1 < rows ? (int)tb[tid + 1] : cnt) - bstart;
+        if (direct && tot == 0) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
+        }
+        s_hist[tid] = bstart;
+        for (int j = (bstart + P - 1) / P; j * P < bstart + tot; ++j) s_piece_bin[j] = tid;
+      }
+      if (tid == 0) s_misc[kFWarps] = cnt;
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        if (cnt == kFTile || j * kFBlock + tid < cnt) {
+          const int pos = (int)((j & 1) ? pw[j / 2] >> 16 : pw[j / 2] & 0xffffu);
+          FC_DCHECK(a, pos >= 0 && pos < cnt);
+          if constexpr (WIDE) {
+            s_sorted[phys(pos)] = make_uint2((uint32_t)comp<W1>(rec[j]), (uint32_t)comp<W2>(rec[j]));
+            s_sval[phys(pos)] = __int_as_float(rec[j].w);
+          } else {
+            const uint32_t pk = ((uint32_t)comp<W1>(rec[j]) << shift) | (uint32_t)comp<W2>(rec[j]);
+            s_sorted[phys(pos)] = make_uint2(pk, (uint32_t)rec[j].w);
+          }
+        }
+      }
+      __syncthreads();
+    } else {
     __syncwarp();
     // ---------------------------------------------------------------- B
     int *wh = s_hist + warp * hstride;
@@ -223,7 +273,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (tid < rows) {
 #pragma unroll 4
         for (int w = 0; w < kFWarps; ++w) tot += s_hist[w * hstride + tid];
-        if (direct && tot == 0) {
+        if (PLAN != 2 && direct && tot == 0) {
           const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
         }
@@ -247,6 +297,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
       if (tid == (one_warp ? 31 : kFBlock - 1)) s_misc[kFWarps] = wpre + incl;
       if (tid < rows) {
         const int bstart = wpre + incl - tot;
+        if constexpr (PLAN == 2) a.plan_bins[tkey * a.hist_rows + tid] = (uint16_t)bstart;
         int base = bstart;
 #pragma unroll 4
         for (int w = 0; w < kFWarps; ++w) {
@@ -266,6 +317,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         const int k = x & 255;
         const int pos = wh[k] + (x >> 8);
         FC_DCHECK(a, k < rows && pos >= 0 && pos < cnt);
+        if constexpr (PLAN == 2) {
+          pw[j / 2] |= (uint32_t)pos << (16 * (j & 1));
+          continue;
+        }
         if constexpr (WIDE) {
           s_sorted[phys(pos)] = make_uint2((uint32_t)comp<W1>(rec[j]), (uint32_t)comp<W2>(rec[j]));
           s_sval[phys(pos)] = __int_as_float(rec[j].w);
@@ -275,13 +330,20 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
         }
       }
     }
+    if constexpr (PLAN == 2) {
+      reinterpret_cast<int4 *>(a.plan_perm + tkey * kFTile)[tid] =
+          make_int4((int)pw[0], (int)pw[1], (int)pw[2], (int)pw[3]);
+    }
     __syncthreads();
+    }
+    if constexpr (PLAN == 2) continue;
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
     if (tid == 0 && t0 + kFTile < end) {
       const int64_t n1 = min64(kFTile, end - (t0 + kFTile));
       prefetch_l2(a.src + (t0 + kFTile), n1 * sizeof(int4));
       if (a.do_remap) prefetch_l2(a.slots + (t0 + kFTile), n1 * sizeof(uint32_t));
+      if constexpr (PLAN == 1) prefetch_l2(a.plan_perm + (tkey + 1) * kFTile, kFTile * sizeof(uint16_t));
     }
     if (lg == 0) {
       s_bnd_row[2 * gi] = -1;
@@ -407,6 +469,7 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
     }
   }
   
+  if constexpr (PLAN == 2) return;
   if (!direct) {
     __syncthreads();
     float *dstp = part < 0 ? out_rows : partial_ws(a, chunk) + (int64_t)part * a.m * R;
@@ -418,10 +481,10 @@ __global__ void __launch_bounds__(kFBlock, PACK_MIN_BLOCKS) mode_pass_pack_kerne
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 }
 
-template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false>
+template <int MODE, int LPG, int RT, bool PEER = false, bool WIDE = false, int PLAN = 0>
 int launch_pack(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = PackPlan<LPG, WIDE>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE>;
+  auto kern = mode_pass_pack_kernel<MODE, LPG, RT, PEER, WIDE, PLAN>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

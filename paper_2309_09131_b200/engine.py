@@ -23,6 +23,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -173,6 +175,77 @@ def check_errors(st: DeviceShardedTensor, next_mode: int | None = None) -> None:
         raise RuntimeError(f"workers processed {processed} of {expected} elements")
 
 
+def tile_plans_wanted(st: DeviceShardedTensor, rank: int) -> bool:
+    """Tile plans cost 2 bytes per nonzero and mode; FLYCOO_TILE_PLAN=0/1
+    forces them off/on, default: on when they fit in a third of the free
+    device memory (config 5's 3.6B nonzeros keep the in-kernel ranking)."""
+    env = os.environ.get("FLYCOO_TILE_PLAN")
+    if env is not None:
+        return env != "0"
+    if st.num_modes != 3 or rank != 32:
+        return False
+    free, _ = torch.cuda.mem_get_info(st.device)
+    return 3 * st.nnz * st.num_modes * 3 < free  # ~3 B per nonzero and mode with partial tiles
+
+
+def build_tile_plans(st: DeviceShardedTensor, rank: int) -> bool:
+    """Emit the tile plan of every mode (fc_tile_plan_emit) by walking the
+    tensor once through its modes with remap-only passes (the layout and the
+    chunk plan are static, so the per-tile sort the mode pass would redo in
+    every sweep is done once here).  Needs the canonical mode-0 arrangement;
+    returns False (and leaves no plan) when the kernels for this tensor do
+    not take one.  The tensor ends as it started."""
+    if st.active_mode != 0 or not st.canonical:
+        raise BufferOrderError("tile plans are emitted from the canonical mode-0 arrangement")
+    L = _lib.load()
+    nmodes, params, dims = st.num_modes, st.params, st.params.dims
+    works = [st.mode_work(n, rank) for n in range(nmodes)]
+    if any(w.tile_perm is not None for w in works):
+        return all(w.tile_perm is not None for w in works)
+    if not all(w.acc_in_smem for w in works):
+        return False
+    check_errors(st)
+    flags_p, proc_p = st.stat_ptrs()
+    strm = _stream()
+    val_p = lambda t: t.data_ptr() if t is not None else None
+    plans = []
+    ok = True
+    for n in range(nmodes):
+        w = works[n]
+        a, b = st.active, 1 - st.active
+        if ok:
+            keys = int(L.fc_tile_plan_keys(st.nnz, w.nchunks))
+            perm = torch.empty(keys * int(L.fc_tile_elems()), dtype=torch.int16, device=st.device)
+            bins = torch.zeros(keys * w.hist_rows, dtype=torch.int16, device=st.device)
+            dummy = _lib.ptr_array([st.crd[a].data_ptr()] * nmodes)  # factor rows are not read
+            rc = L.fc_tile_plan_emit(
+                st.crd[a].data_ptr(), val_p(st.val[a]), dummy, _lib.i64_array(dims), nmodes, n, rank,
+                dims[n], params.m[n], w.chunk_start.data_ptr(), w.chunk_ss.data_ptr(),
+                w.chunk_part.data_ptr(),
+                w.chunk_rows.data_ptr() if w.chunk_rows is not None else None,
+                w.tile_rows, w.hist_rows, w.nchunks, st.nnz, flags_p, proc_p, perm.data_ptr(),
+                bins.data_ptr(), strm)
+            if rc == _lib.ERR_UNSUPPORTED:
+                ok = False
+            elif rc != 0:
+                raise _lib.FlycooError(
+                    f"fc_tile_plan_emit failed ({rc}): {L.fc_last_error().decode(errors='replace')}")
+            else:
+                plans.append((perm, bins))
+        # on to the next mode's arrangement: remap only
+        _lib.call("fc_mode_worker", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
+                  val_p(st.val[b]), None, None, None, nmodes, n, rank, dims[n], params.m[n],
+                  None, None, None, None, 0, 0, 0, None, 0, None, 0, None, None,
+                  st.slot_maps[n].data_ptr(), st.nnz, 0, 1, 1, flags_p, proc_p, strm)
+        st._expected += st.nnz
+        st.swap((n + 1) % nmodes, still_canonical=True)
+    check_errors(st)
+    if ok:
+        for w, (perm, bins) in zip(works, plans):
+            w.tile_perm, w.tile_bins = perm, bins
+    return ok
+
+
 def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int | None = None,
                 remap: str = "slot", counters: TrafficCounters | None = None,
                 split_remap: bool = False, alloc_log: dict | None = None, *,
@@ -206,6 +279,12 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
 
     L = _lib.load()
     work = st.mode_work(mode, rank)
+    if (work.tile_perm is None and mode == 0 and st.canonical and not st._tile_plans_tried.get(rank)
+            and remap == "slot"):
+        # first pass over a fresh tensor: the static per-tile sort is planned once
+        st._tile_plans_tried[rank] = True
+        if tile_plans_wanted(st, rank):
+            build_tile_plans(st, rank)
     dims = params.dims
     out = (torch.empty if work.acc_in_smem else torch.zeros)(
         (dims[mode], rank), dtype=torch.float32, device=st.device)
@@ -232,6 +311,22 @@ def mttkrp_mode(st: DeviceShardedTensor, factors, mode: int, smap, workers: int 
     passes = [(True, False)] if use_cursor else ref_passes
     val_p = lambda t: t.data_ptr() if t is not None else None
     for do_compute, do_remap in passes:
+        if do_compute and work.tile_perm is not None and st.canonical:
+            # the planned pass: sorted positions and bin starts come from the tile plan
+            _lib.call("fc_mode_worker_planned", st.crd[a].data_ptr(), val_p(st.val[a]),
+                      st.crd[b].data_ptr(), val_p(st.val[b]), fptrs, _lib.i64_array(params.dims),
+                      out.data_ptr(), nmodes, mode, rank, dims[mode], params.m[mode],
+                      work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),
+                      work.chunk_part.data_ptr(),
+                      work.chunk_rows.data_ptr() if work.chunk_rows is not None else None,
+                      work.tile_rows, work.hist_rows, work.nchunks, work.red1.data_ptr(),
+                      work.nred1, work.red2.data_ptr(), work.nred2,
+                      work.part_ws.data_ptr() if work.part_ws is not None else None,
+                      work.part_ws2.data_ptr() if work.part_ws2 is not None else None,
+                      st.slot_maps[mode].data_ptr(), st.nnz, int(do_remap), flags_p, proc_p,
+                      work.tile_perm.data_ptr(), work.tile_bins.data_ptr(), strm)
+            st._expected += st.nnz
+            continue
         _lib.call("fc_mode_worker", st.crd[a].data_ptr(), val_p(st.val[a]), st.crd[b].data_ptr(),
                   val_p(st.val[b]), fptrs, _lib.i64_array(params.dims), out.data_ptr(), nmodes, mode, rank, dims[mode],
                   params.m[mode], work.chunk_start.data_ptr(), work.chunk_ss.data_ptr(),

@@ -121,6 +121,10 @@ class ModeWork:
     part_ws: torch.Tensor | None
     part_ws2: torch.Tensor | None
     chunk_elems: int
+    # tile plan (engine.build_tile_plans): every element's position in its
+    # row-sorted 2048-element tile and every tile's bin starts, uint16 bits
+    tile_perm: torch.Tensor | None = None
+    tile_bins: torch.Tensor | None = None
 
     @property
     def launches(self) -> int:
@@ -323,6 +327,7 @@ class DeviceShardedTensor:
         self.active_mode = 0
         self.canonical = True
         self._work = {}
+        self._tile_plans_tried = {}  # rank -> tile plans were considered (engine.build_tile_plans)
         # [processed elements, error flags] for the deferred end-of-pass checks
         self._stat = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._expected = 0
