@@ -14,9 +14,9 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     // 8-byte sorted records when the two input coordinates fit 32 bits
     const KernelVariant &kv = kernel_variant();
     if (a.plan) {
-      // tile plan: the R = 32 packed kernels of one GPU (tile keys: t0 / kTile + chunk)
+      // tile plan: the R = 32 / R = 16 packed kernels of one GPU (tile keys: t0 / kTile + chunk)
       static_assert(kFTile == kTile, "the tile plan is indexed by 2048-element tiles");
-      if constexpr (RT == 32 && !PEER) {
+      if constexpr ((RT == 32 || RT == 16) && !PEER) {
         if (a.pack_shift > 0 && kv.pack)
           return a.plan == 1 ? launch_pack<MODE, LPG, RT, false, false, 1>(a, nchunks, st)
                              : launch_pack<MODE, LPG, RT, false, false, 2>(a, nchunks, st);

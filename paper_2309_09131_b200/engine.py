@@ -182,7 +182,7 @@ def tile_plans_wanted(st: DeviceShardedTensor, rank: int) -> bool:
     env = os.environ.get("FLYCOO_TILE_PLAN")
     if env is not None:
         return env != "0"
-    if st.num_modes != 3 or rank != 32:
+    if st.num_modes != 3 or rank not in (16, 32):
         return False
     free, _ = torch.cuda.mem_get_info(st.device)
     return 3 * st.nnz * st.num_modes * 3 < free  # ~3 B per nonzero and mode with partial tiles

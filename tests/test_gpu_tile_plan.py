@@ -59,6 +59,27 @@ def test_planned_sweeps_equal_ranked_sweeps(name, monkeypatch):
         assert torch.equal(st.crd[st.active], ref.crd[ref.active]), (name, rep)
 
 
+def test_planned_rank16_equals_ranked(monkeypatch):
+    from paper_2309_09131_b200 import (DeviceFactorSet, build_device_sharded, device_params,
+                                       schedule_super_shards, sweep_all_modes)
+    from paper_2309_09131_b200.synth import zipf_tensor
+    dims = (1000, 800, 600)
+    coords, vals = zipf_tensor(dims, 300_000, seed=6, exponents=(None, None, None))
+    params = device_params(dims, 300_000, 16)
+    monkeypatch.setenv("FLYCOO_TILE_PLAN", "0")
+    ref = build_device_sharded(coords, vals, params)
+    smap = schedule_super_shards(ref.plan, 1)
+    fs = DeviceFactorSet.random_device(dims, 16, seed=3)
+    want = sweep_all_modes(ref, fs, smap)
+    monkeypatch.setenv("FLYCOO_TILE_PLAN", "1")
+    st = build_device_sharded(coords, vals, params)
+    got = sweep_all_modes(st, fs, smap)  # planned on its first mode-0 pass
+    assert all(st.mode_work(n, 16).tile_perm is not None for n in range(3))
+    for a, b in zip(got.factors, want.factors):
+        assert torch.equal(a, b)
+    assert torch.equal(st.crd[st.active], ref.crd[ref.active])
+
+
 def test_planned_mode_passes_match_the_oracle():
     from paper_2309_09131_b200 import DeviceFactorSet, mttkrp_mode
     c = CASES["packed"]
@@ -74,7 +95,7 @@ def test_planned_mode_passes_match_the_oracle():
 
 
 def test_plan_is_skipped_where_it_does_not_apply(monkeypatch):
-    """R = 16 and 4-mode tensors keep the in-kernel ranking; a cursor-remapped
+    """Ranks other than 16 / 32 keep the in-kernel ranking; a cursor-remapped
     (non-canonical) buffer does not use a plan emitted for the canonical order."""
     from paper_2309_09131_b200 import (DeviceFactorSet, build_device_sharded, device_params,
                                        mttkrp_mode, schedule_super_shards, sweep_all_modes)
@@ -83,11 +104,11 @@ def test_plan_is_skipped_where_it_does_not_apply(monkeypatch):
     monkeypatch.setenv("FLYCOO_TILE_PLAN", "1")
     dims = (3000, 2000, 2500)
     coords, vals = zipf_tensor(dims, 200_000, seed=5, exponents=(1.1,) * 3)
-    st16 = build_device_sharded(coords, vals, device_params(dims, 200_000, 16, g=4096))
-    assert not build_tile_plans(st16, 16)
-    smap16 = schedule_super_shards(st16.plan, 1)
-    sweep_all_modes(st16, DeviceFactorSet.random_device(dims, 16, seed=1), smap16)
-    assert all(w.tile_perm is None for w in st16._work.values())
+    st8 = build_device_sharded(coords, vals, device_params(dims, 200_000, 8, g=4096))
+    assert not build_tile_plans(st8, 8)
+    smap8 = schedule_super_shards(st8.plan, 1)
+    sweep_all_modes(st8, DeviceFactorSet.random_device(dims, 8, seed=1), smap8)
+    assert all(w.tile_perm is None for w in st8._work.values())
 
     params = device_params(dims, 200_000, 32, g=4096)
     st = build_device_sharded(coords, vals, params)
