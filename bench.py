@@ -197,10 +197,12 @@ def kernel_names(params, works, rank: int) -> list:
         elif N == 3 and os.environ.get("FLYCOO_PACK") != "0":
             w1, w2 = (1, 2) if n == 0 else (0, 2) if n == 1 else (0, 1)
             b1, b2 = ((dims[w1] - 1).bit_length(), (dims[w2] - 1).bit_length())
+            planned = ", tile plan: sorted positions and bin starts read, not ranked" \
+                if getattr(w, "tile_perm", None) is not None else ""
             if b2 >= 1 and b1 + b2 <= 32:
-                names.append("mode_pass_pack_kernel (8-B sorted records)")
+                names.append(f"mode_pass_pack_kernel (8-B sorted records{planned})")
             elif os.environ.get("FLYCOO_PACK_WIDE") != "0":
-                names.append("mode_pass_pack_kernel WIDE ({c_w1, c_w2} + value)")
+                names.append(f"mode_pass_pack_kernel WIDE ({{c_w1, c_w2}} + value{planned})")
             else:
                 names.append("mode_pass_fast_kernel")
         else:
@@ -667,6 +669,11 @@ def run_ours(args, rank, world, local):
                                  "lean (bucketed generator, layout.build_device_sharded_lean)"
                                  if lean else "regular"),
                        "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2),
+                       # static per-tile sort emitted once (engine.build_tile_plans), bytes held
+                       "tile_plan_bytes": sum(
+                           (w.tile_perm.numel() + w.tile_bins.numel()) * 2
+                           for w in (src.mode_work(n, R) for n in range(N))
+                           if getattr(w, "tile_perm", None) is not None),
                        # SURVEY 8(d) also asks for nnz / t_sweep (value is N * nnz / t_sweep)
                        "nnz_per_s_sweep": nnz / (ms_per_step / 1e3),
                        # median over the measured sweeps of each mode pass
