@@ -184,8 +184,11 @@ def tile_plans_wanted(st: DeviceShardedTensor, rank: int) -> bool:
         return env != "0"
     if st.num_modes != 3 or rank not in (16, 32):
         return False
+    # ~3 B per nonzero and mode with partial tiles; memory the caching
+    # allocator holds but does not use counts as free
     free, _ = torch.cuda.mem_get_info(st.device)
-    return 3 * st.nnz * st.num_modes * 3 < free  # ~3 B per nonzero and mode with partial tiles
+    free += torch.cuda.memory_reserved(st.device) - torch.cuda.memory_allocated(st.device)
+    return 3 * (3 * st.nnz * st.num_modes) < free
 
 
 def build_tile_plans(st: DeviceShardedTensor, rank: int) -> bool:
