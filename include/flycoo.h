@@ -126,7 +126,8 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
  * fc_mode_worker (do_compute = 1, shared-memory accumulation) reading that
  * plan instead of ranking: same sorted order, hence bitwise the same sums.
  * Both return FC_ERR_UNSUPPORTED outside the kernels that take a plan
- * (3-mode tensors at R = 32 or 16, one GPU); callers then use fc_mode_worker.
+ * (3-mode tensors at R = 32 or 16, 4-mode tensors at R = 32; one GPU);
+ * callers then use fc_mode_worker.
  * The plan is valid for the work plan (chunk arrays) it was emitted with and
  * for the canonical (slot-remapped) order only. */
 int fc_tile_plan_emit(const void *src_crd, const float *src_val,

@@ -30,7 +30,14 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     // wider coordinates: {c_w1, c_w2} + value array, rows from the bins
     if (a.pack_shift == 0 && kv.pack_wide) return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
-  if (a.plan) return FC_ERR_UNSUPPORTED;
+  if (a.plan) {  // the 4-mode tile kernels at R = 32 take a plan too
+    if constexpr (NM == 4 && RT == 32 && !PEER) {
+      static_assert(kFTile == kTile, "the tile plan is indexed by 2048-element tiles");
+      return a.plan == 1 ? launch_fast<NM, MODE, LPG, RT, false, 1>(a, nchunks, st)
+                         : launch_fast<NM, MODE, LPG, RT, false, 2>(a, nchunks, st);
+    }
+    return FC_ERR_UNSUPPORTED;
+  }
   return launch_fast<NM, MODE, LPG, RT, PEER>(a, nchunks, st);
 }
 

@@ -137,7 +137,10 @@ __device__ __forceinline__ void element_term(const ModeArgs &a, int R, int col, 
   for (int k = 0; k < 4; ++k) t[k] = v * pr[k];
 }
 
-template <int NM, int MODE, int LPG, int RT, bool PEER = false>
+// PLAN: 0 = rank every tile in the kernel; 1 = sorted positions (and, for
+// direct chunks, bin starts) from the tile plan; 2 = rank and write the plan
+// (nothing else) -- see pack_kernel.cuh.
+template <int NM, int MODE, int LPG, int RT, bool PEER = false, int PLAN = 0>
 __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kernel(const __grid_constant__ ModeArgs a) {
   using FP = FastPlan<NM, LPG>;
   constexpr int G = FP::G;
@@ -177,7 +180,9 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   // complete inside the tile and is stored straight to `out` (no tile acc)
   const bool direct = part == kPartDirect;
   float *out_rows = a.out + row0 * R;
-  if (direct) {
+  if (PLAN == 2) {
+    if (start == end) return;
+  } else if (direct) {
     if (start == end) {  // only empty super-shards: their rows are zero
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int i = tid; i < rows * R / 4; i += kFBlock) reinterpret_cast<float4 *>(out_rows)[i] = z;
@@ -203,6 +208,14 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
     int4 rec[kFIPT];
     float rv[kFIPT];
     uint32_t slot[kFIPT];
+    // tile plan: this tile's key, the thread's 8 sorted positions in one word
+    const int64_t tkey = t0 / kFTile + chunk;
+    static_assert(PLAN == 0 || kFIPT == 8, "the tile plan packs 8 positions per thread");
+    uint32_t pw[PLAN != 0 ? 4 : 1] = {};
+    if constexpr (PLAN == 1) {
+      const int4 w4 = ld_stream_v4(reinterpret_cast<const int4 *>(a.plan_perm + tkey * kFTile) + tid);
+      pw[0] = (uint32_t)w4.x, pw[1] = (uint32_t)w4.y, pw[2] = (uint32_t)w4.z, pw[3] = (uint32_t)w4.w;
+    }
     if (cnt == kFTile) {  // full tile: no per-item bounds test
 #pragma unroll
       for (int j = 0; j < kFIPT; ++j) {
@@ -226,7 +239,9 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         }
       }
     }
-    for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
+    if constexpr (PLAN != 1) {
+      for (int b = lane; b < rows; b += 32) s_hist[warp * hstride + b] = 0;
+    }
 #pragma unroll
     for (int j = 0; j < kFIPT; ++j) {
       const int e = j * kFBlock + tid;
@@ -234,9 +249,30 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         if (a.do_remap) {
           remap_store<1, EMB, PEER>(a, slot[j], rec[j], rec[j], EMB ? 0.f : rv[j]);
         }
-        if (key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
+        if (PLAN != 1 && key_of(rec[j]) < 0) atomicOr(a.flags, FC_FLAG_ROW_OUTSIDE_SS);
       }
     }
+    if constexpr (PLAN == 1) {
+      // ------------------------------------------------------------ B (planned)
+      if (direct && tid < rows) {  // empty rows of a direct chunk are zero
+        const uint16_t *tb = a.plan_bins + tkey * a.hist_rows;
+        if ((tid + 1 < rows ? (int)tb[tid + 1] : cnt) == (int)tb[tid]) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
+        }
+      }
+      if (tid == 0) s_misc[kFWarps] = cnt;
+#pragma unroll
+      for (int j = 0; j < kFIPT; ++j) {
+        if (cnt == kFTile || j * kFBlock + tid < cnt) {
+          const int pos = (int)((j & 1) ? pw[j / 2] >> 16 : pw[j / 2] & 0xffffu);
+          FC_DCHECK(a, pos >= 0 && pos < cnt);
+          s_sorted[phys(pos)] = rec[j];
+          if (!EMB) s_sval[phys(pos)] = rv[j];
+        }
+      }
+      __syncthreads();
+    } else {
     __syncwarp();
     // ---------------------------------------------------------------- B
     {
@@ -301,7 +337,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       if (tid < rows) {
 #pragma unroll 4
         for (int w = 0; w < kFWarps; ++w) tot += s_hist[w * hstride + tid];
-        if (direct && tot == 0) {
+        if (PLAN != 2 && direct && tot == 0) {
           const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int c = 0; c < R; c += 4) *reinterpret_cast<float4 *>(out_rows + tid * R + c) = z;
         }
@@ -320,6 +356,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       if (tid == kFBlock - 1) s_misc[kFWarps] = wpre + incl;
       if (tid < rows) {
         int base = wpre + incl - tot;
+        if constexpr (PLAN == 2) a.plan_bins[tkey * a.hist_rows + tid] = (uint16_t)base;
 #pragma unroll 4
         for (int w = 0; w < kFWarps; ++w) {
           const int c = s_hist[w * hstride + tid];
@@ -336,13 +373,23 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
         const int k = x & 255;
         const int pos = wh[k] + (x >> 8);
         FC_DCHECK(a, k < rows && pos >= 0 && pos < cnt);
+        if constexpr (PLAN == 2) {
+          pw[j / 2] |= (uint32_t)pos << (16 * (j & 1));
+          continue;
+        }
         set_comp<MODE>(rec[j], irow0 + k);
         s_sorted[phys(pos)] = rec[j];
         if (!EMB) s_sval[phys(pos)] = rv[j];
       }
     }
+    if constexpr (PLAN == 2) {
+      reinterpret_cast<int4 *>(a.plan_perm + tkey * kFTile)[tid] =
+          make_int4((int)pw[0], (int)pw[1], (int)pw[2], (int)pw[3]);
+    }
     __syncthreads();
     }
+    }
+    if constexpr (PLAN == 2) continue;
     const int nvalid = s_misc[kFWarps];
     // ---------------------------------------------------------------- C
     if (tid == 0 && t0 + kFTile < end) {  // next tile's records + slots -> L2
@@ -350,6 +397,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       prefetch_l2(a.src + (t0 + kFTile), n1 * sizeof(int4));
       if (a.do_remap) prefetch_l2(a.slots + (t0 + kFTile), n1 * sizeof(uint32_t));
       if (!EMB) prefetch_l2(a.src_val + (t0 + kFTile), n1 * sizeof(float));
+      if constexpr (PLAN == 1) prefetch_l2(a.plan_perm + (tkey + 1) * kFTile, kFTile * sizeof(uint16_t));
     }
     // both boundary entries of every group are (re)written this tile: rows
     // -1 and zero vectors unless a segment lands there
@@ -451,6 +499,7 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
       }
     }
   }
+  if constexpr (PLAN == 2) return;
   if (!direct) {
     __syncthreads();
     float *dstp = part < 0 ? out_rows : partial_ws(a, chunk) + (int64_t)part * a.m * R;
@@ -462,10 +511,10 @@ __global__ void __launch_bounds__(kFBlock, FAST_MIN_BLOCKS) mode_pass_fast_kerne
   if (tid == 0) atomicAdd(a.counters, (unsigned long long)(end - start));
 }
 
-template <int NM, int MODE, int LPG, int RT, bool PEER = false>
+template <int NM, int MODE, int LPG, int RT, bool PEER = false, int PLAN = 0>
 int launch_fast(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
   const size_t smem = FastPlan<NM, LPG>::total(a.rank, a.tile_rows, a.hist_rows);
-  auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT, PEER>;
+  auto kern = mode_pass_fast_kernel<NM, MODE, LPG, RT, PEER, PLAN>;
   static size_t configured = 0;
   if (smem > configured) {
     FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

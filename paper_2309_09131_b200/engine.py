@@ -182,7 +182,7 @@ def tile_plans_wanted(st: DeviceShardedTensor, rank: int) -> bool:
     env = os.environ.get("FLYCOO_TILE_PLAN")
     if env is not None:
         return env != "0"
-    if st.num_modes != 3 or rank not in (16, 32):
+    if not ((st.num_modes == 3 and rank in (16, 32)) or (st.num_modes == 4 and rank == 32)):
         return False
     # ~3 B per nonzero and mode with partial tiles; memory the caching
     # allocator holds but does not use counts as free

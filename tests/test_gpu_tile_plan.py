@@ -30,6 +30,8 @@ CASES = {
     "direct": dict(dims=(400_000, 300, 200), nnz=400_000, law=(1.0, 1.1, 1.1), kw=dict(g=2048)),
     # 46 rows in mode 0: two super-shards holding everything (heavy rows)
     "heavy": dict(dims=(46, 20_000, 20_000), nnz=700_000, law=(None, 1.0, 1.0), kw=dict(g=8192)),
+    # 4 modes (tile kernel, separate value array), one of them sparse (direct chunks)
+    "four": dict(dims=(5000, 300_000, 4000, 90), nnz=500_000, law=(1.2, 1.2, 1.2, 1.2), kw=dict(g=4096)),
 }
 
 
@@ -49,7 +51,7 @@ def test_planned_sweeps_equal_ranked_sweeps(name, monkeypatch):
     assert build_tile_plans(st, 32)
     assert st.active_mode == 0 and st.canonical
     assert torch.equal(st.crd[st.active], before)  # the emission walk returns to mode 0
-    assert all(st.mode_work(n, 32).tile_perm is not None for n in range(3))
+    assert all(st.mode_work(n, 32).tile_perm is not None for n in range(len(c["dims"])))
     for rep in range(2):  # both buffer parities
         got = sweep_all_modes(st, fs, smap)
         if rep:
