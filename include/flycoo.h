@@ -126,8 +126,8 @@ int fc_mode_worker(const void *src_crd, const float *src_val,
  * fc_mode_worker (do_compute = 1, shared-memory accumulation) reading that
  * plan instead of ranking: same sorted order, hence bitwise the same sums.
  * Both return FC_ERR_UNSUPPORTED outside the kernels that take a plan
- * (3-mode tensors at R = 32 or 16, 4-mode tensors at R = 32; one GPU);
- * callers then use fc_mode_worker.
+ * (3-mode tensors at R = 32 or 16, 4-mode tensors at R = 32); callers then
+ * use fc_mode_worker.
  * The plan is valid for the work plan (chunk arrays) it was emitted with and
  * for the canonical (slot-remapped) order only. */
 int fc_tile_plan_emit(const void *src_crd, const float *src_val,
@@ -182,6 +182,25 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val,
                          int npeers, void *const *peer_crd, float *const *peer_val,
                          const int64_t *peer_base, float *const *peer_part_ws,
                          const int32_t *chunk_owner, void *stream);
+/* fc_mode_worker_peers reading a tile plan emitted on this GPU's slice
+ * (fc_tile_plan_emit with the same shifted pointers and chunk range; keys
+ * t0 / 2048 + local chunk index, t0 the global element index); tile_perm
+ * NULL: rank in the kernel. */
+int fc_mode_worker_peers_planned(const void *src_crd, const float *src_val,
+                         const float *const *factors, const int64_t *dims,
+                         float *out, int nmodes, int mode, int rank,
+                         int64_t out_rows, int64_t m_mode,
+                         const int64_t *chunk_start, const int32_t *chunk_ss,
+                         const int32_t *chunk_part, const int32_t *chunk_rows,
+                         int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                         const int64_t *red1, int64_t nred1, const int64_t *red2,
+                         int64_t nred2, float *part_ws, float *part_ws2,
+                         const uint32_t *dest_slots, int64_t nnz, int do_compute,
+                         int acc_in_smem, int32_t *flags, unsigned long long *counters,
+                         int npeers, void *const *peer_crd, float *const *peer_val,
+                         const int64_t *peer_base, float *const *peer_part_ws,
+                         const int32_t *chunk_owner, const uint16_t *tile_perm, const uint16_t *tile_bins,
+                         void *stream);
 
 /* K2 alone (the second half of fc_mode_worker): the deterministic two-level
  * reduce of partial tiles into `out`.  Multi-GPU: the owner of super-shards

@@ -55,6 +55,20 @@ _SIGS = {
         _vp, _vp,                      # flags, counters
         _int, _vp, _vp, _vp,           # npeers, peer_crd, peer_val (host arrays), peer_base (host)
         _vp, _vp,                      # peer_part_ws (host array), chunk_owner (device int32)
+        _vp]),
+    "fc_mode_worker_peers_planned": (_int, [
+        _vp, _vp,                      # src_crd, src_val
+        _vp, _vp, _vp,                 # factors (host array of device ptrs), dims (host), out
+        _int, _int, _int,              # nmodes, mode, rank
+        _i64, _i64,                    # out_rows, m_mode
+        _vp, _vp, _vp, _vp, _i64, _i64, _i64,  # chunk_start/ss/part/rows, tile_rows, hist_rows, nchunks
+        _vp, _i64, _vp, _i64,          # red1, nred1, red2, nred2
+        _vp, _vp, _vp, _i64,           # part_ws, part_ws2, dest_slots (global), nnz (local)
+        _int, _int,                    # do_compute, acc_in_smem
+        _vp, _vp,                      # flags, counters
+        _int, _vp, _vp, _vp,           # npeers, peer_crd, peer_val (host arrays), peer_base (host)
+        _vp, _vp,                      # peer_part_ws (host array), chunk_owner (device int32)
+        _vp, _vp,                      # tile_perm, tile_bins (device uint16, or NULL)
         _vp]),                         # stream
     "fc_reduce_partials": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "fc_tile_plan_emit": (_int, [

@@ -16,13 +16,16 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     if (a.plan) {
       // tile plan: the R = 32 / R = 16 packed kernels of one GPU (tile keys: t0 / kTile + chunk)
       static_assert(kFTile == kTile, "the tile plan is indexed by 2048-element tiles");
-      if constexpr ((RT == 32 || RT == 16) && !PEER) {
-        if (a.pack_shift > 0 && kv.pack)
-          return a.plan == 1 ? launch_pack<MODE, LPG, RT, false, false, 1>(a, nchunks, st)
-                             : launch_pack<MODE, LPG, RT, false, false, 2>(a, nchunks, st);
-        if (a.pack_shift == 0 && kv.pack_wide)
-          return a.plan == 1 ? launch_pack<MODE, LPG, RT, false, true, 1>(a, nchunks, st)
-                             : launch_pack<MODE, LPG, RT, false, true, 2>(a, nchunks, st);
+      // (the emission pass, plan == 2, never remaps: single-GPU instances only)
+      if constexpr (RT == 32 || RT == 16) {
+        if (a.pack_shift > 0 && kv.pack) {
+          if (a.plan == 1) return launch_pack<MODE, LPG, RT, PEER, false, 1>(a, nchunks, st);
+          if constexpr (!PEER) return launch_pack<MODE, LPG, RT, false, false, 2>(a, nchunks, st);
+        }
+        if (a.pack_shift == 0 && kv.pack_wide) {
+          if (a.plan == 1) return launch_pack<MODE, LPG, RT, PEER, true, 1>(a, nchunks, st);
+          if constexpr (!PEER) return launch_pack<MODE, LPG, RT, false, true, 2>(a, nchunks, st);
+        }
       }
       return FC_ERR_UNSUPPORTED;
     }
@@ -31,10 +34,10 @@ int launch_choice(const ModeArgs &a, int64_t nchunks, cudaStream_t st) {
     if (a.pack_shift == 0 && kv.pack_wide) return launch_pack<MODE, LPG, RT, PEER, true>(a, nchunks, st);
   }
   if (a.plan) {  // the 4-mode tile kernels at R = 32 take a plan too
-    if constexpr (NM == 4 && RT == 32 && !PEER) {
+    if constexpr (NM == 4 && RT == 32) {
       static_assert(kFTile == kTile, "the tile plan is indexed by 2048-element tiles");
-      return a.plan == 1 ? launch_fast<NM, MODE, LPG, RT, false, 1>(a, nchunks, st)
-                         : launch_fast<NM, MODE, LPG, RT, false, 2>(a, nchunks, st);
+      if (a.plan == 1) return launch_fast<NM, MODE, LPG, RT, PEER, 1>(a, nchunks, st);
+      if constexpr (!PEER) return launch_fast<NM, MODE, LPG, RT, false, 2>(a, nchunks, st);
     }
     return FC_ERR_UNSUPPORTED;
   }

@@ -607,7 +607,7 @@ static int mode_worker_impl(const void *src_crd, const float *src_val, void *dst
   a.plan = plan;
   if (plan) {
     FC_CHECK_ARG(plan_perm && plan_bins, "null tile plan");
-    if (!acc_in_smem || !fast_ok(a, true) || peers.n > 0) return FC_ERR_UNSUPPORTED;
+    if (!acc_in_smem || !fast_ok(a, true) || (plan == 2 && peers.n > 0)) return FC_ERR_UNSUPPORTED;
   }
   int rc = acc_in_smem ? dispatch<true>(a, nchunks, st) : dispatch<false>(a, nchunks, st);
   if (rc != FC_OK) return rc;
@@ -698,6 +698,29 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float 
                          int npeers, void *const *peer_crd, float *const *peer_val,
                          const int64_t *peer_base, float *const *peer_part_ws,
                          const int32_t *chunk_owner, void *stream) {
+  return fc_mode_worker_peers_planned(src_crd, src_val, factors, dims, out, nmodes, mode, rank,
+                                      out_rows, m_mode, chunk_start, chunk_ss, chunk_part,
+                                      chunk_rows, tile_rows, hist_rows, nchunks, red1, nred1, red2,
+                                      nred2, part_ws, part_ws2, dest_slots, nnz, do_compute,
+                                      acc_in_smem, flags, counters, npeers, peer_crd, peer_val,
+                                      peer_base, peer_part_ws, chunk_owner, nullptr, nullptr,
+                                      stream);
+}
+
+int fc_mode_worker_peers_planned(const void *src_crd, const float *src_val,
+                                 const float *const *factors, const int64_t *dims, float *out,
+                                 int nmodes, int mode, int rank, int64_t out_rows, int64_t m_mode,
+                                 const int64_t *chunk_start, const int32_t *chunk_ss,
+                                 const int32_t *chunk_part, const int32_t *chunk_rows,
+                                 int64_t tile_rows, int64_t hist_rows, int64_t nchunks,
+                                 const int64_t *red1, int64_t nred1, const int64_t *red2,
+                                 int64_t nred2, float *part_ws, float *part_ws2,
+                                 const uint32_t *dest_slots, int64_t nnz, int do_compute,
+                                 int acc_in_smem, int32_t *flags, unsigned long long *counters,
+                                 int npeers, void *const *peer_crd, float *const *peer_val,
+                                 const int64_t *peer_base, float *const *peer_part_ws,
+                                 const int32_t *chunk_owner, const uint16_t *tile_perm,
+                                 const uint16_t *tile_bins, void *stream) {
   FC_CHECK_ARG(npeers >= 1 && npeers <= kMaxPeers, "npeers %d outside [1, %d]", npeers, kMaxPeers);
   FC_CHECK_ARG(peer_crd && peer_base && (dest_slots || nnz == 0), "null peer table");
   PeerTable t{};
@@ -721,7 +744,8 @@ int fc_mode_worker_peers(const void *src_crd, const float *src_val, const float 
                           rank, out_rows, m_mode, chunk_start, chunk_ss, chunk_part, chunk_rows,
                           tile_rows, hist_rows, nchunks, red1, nred1, red2, nred2, part_ws,
                           part_ws2, dest_slots, nnz, do_compute, 1, acc_in_smem, flags, counters,
-                          stream, t, chunk_owner);
+                          stream, t, chunk_owner, const_cast<uint16_t *>(tile_perm),
+                          const_cast<uint16_t *>(tile_bins), tile_perm && do_compute ? 1 : 0);
 }
 
 int fc_reduce_partials(const int64_t *red1, int64_t nred1, const int64_t *red2, int64_t nred2,

@@ -273,6 +273,7 @@ class PeerShardedTensor:
             w.part_ws = None
         self.active = 0
         self.active_mode = 0
+        self._tile_plans = {}    # mode -> (perm, bins, shifted pointers) or None (_tile_plan)
         self.peer_crd = None     # [buffer k][rank q] -> device pointer
         self.peer_val = None
         self.peer_part_ws = None
@@ -408,6 +409,7 @@ class PeerShardedTensor:
         srcv = None if self.val[a] is None else self.val[a].data_ptr() - p.e_lo * 4
         slots = p.global_slots.data_ptr() - p.e_lo * 4 if p.count else None
         pv = None if self.peer_val is None else _lib.ptr_array(self.peer_val[b])
+        plan = self._tile_plan(mode, w, p, src, srcv, factors, R, stat, st)
         if not w.acc_in_smem:
             # the general kernel accumulates straight into `out` (one chunk
             # per super-shard, owned by this GPU): the owned rows start at 0
@@ -416,7 +418,7 @@ class PeerShardedTensor:
             if hi > lo:
                 with torch.cuda.stream(torch.cuda.ExternalStream(st, device=self.device)):
                     out[lo:hi].zero_()
-        _lib.call("fc_mode_worker_peers", src, srcv,
+        _lib.call("fc_mode_worker_peers_planned", src, srcv,
                   _lib.ptr_array([f.data_ptr() for f in factors]), _lib.i64_array(params.dims),
                   out.data_ptr(), self.num_modes, mode, R, params.dims[mode], params.m[mode],
                   w.chunk_start.data_ptr() + 8 * c0, w.chunk_ss.data_ptr() + 4 * c0,
@@ -426,8 +428,56 @@ class PeerShardedTensor:
                   self.part_ws.data_ptr(), None, slots, p.count, 1, int(w.acc_in_smem),
                   stat + 8, stat, self.world, _lib.ptr_array(self.peer_crd[b]), pv,
                   _lib.i64_array(p.peer_base), _lib.ptr_array(self.peer_part_ws),
-                  p.chunk_owner.data_ptr() if p.chunk_owner.numel() else None, st)
+                  p.chunk_owner.data_ptr() if p.chunk_owner.numel() else None,
+                  plan[2] if plan else None, plan[3] if plan else None, st)
         self._expected += p.count
+
+    def _tile_plan(self, mode, w, p, src, srcv, factors, R, stat, st):
+        """This GPU's tile plan of `mode` (engine.build_tile_plans for a slice):
+        emitted on the first pass over the mode -- the slice is in its
+        canonical order then and in every later sweep -- with the same
+        shifted pointers and chunk range the mode pass uses.  Returns the
+        tensors and their key-shifted pointers, or None (no plan: the kernel
+        ranks)."""
+        if mode in self._tile_plans:
+            return self._tile_plans[mode]
+        self._tile_plans[mode] = None
+        env = os.environ.get("FLYCOO_TILE_PLAN")
+        N = self.num_modes
+        if (env == "0" or not w.acc_in_smem or p.count == 0
+                or not ((N == 3 and R in (16, 32)) or (N == 4 and R == 32))):
+            return None
+        L = _lib.load()
+        tile = int(L.fc_tile_elems())
+        nch = p.c_hi - p.c_lo
+        k0 = p.e_lo // tile  # first tile key of the slice (keys: global t0 // tile + local chunk)
+        keys = (p.e_hi - 1) // tile - k0 + nch + 2
+        if env is None:
+            free, _ = torch.cuda.mem_get_info(self.device)
+            free += torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+            if 3 * keys * (tile + w.hist_rows) * 2 * N > free:
+                return None
+        perm = torch.empty(keys * tile, dtype=torch.int16, device=self.device)
+        bins = torch.zeros(keys * w.hist_rows, dtype=torch.int16, device=self.device)
+        perm_p = perm.data_ptr() - k0 * tile * 2
+        bins_p = bins.data_ptr() - k0 * w.hist_rows * 2
+        params = self.plan.params
+        c0 = p.c_lo
+        with torch.cuda.stream(torch.cuda.ExternalStream(st, device=self.device)):
+            rc = L.fc_tile_plan_emit(
+                src, srcv, _lib.ptr_array([f.data_ptr() for f in factors]),
+                _lib.i64_array(params.dims), N, mode, R, params.dims[mode], params.m[mode],
+                w.chunk_start.data_ptr() + 8 * c0, w.chunk_ss.data_ptr() + 4 * c0,
+                w.chunk_part.data_ptr() + 4 * c0,
+                None if w.chunk_rows is None else w.chunk_rows.data_ptr() + 4 * c0,
+                w.tile_rows, w.hist_rows, nch, p.count, stat + 8, stat, perm_p, bins_p, st)
+        if rc == _lib.ERR_UNSUPPORTED:
+            return None
+        if rc != 0:
+            raise _lib.FlycooError(
+                f"fc_tile_plan_emit failed ({rc}): {L.fc_last_error().decode(errors='replace')}")
+        self._tile_plans[mode] = (perm, bins, perm_p, bins_p)
+        return self._tile_plans[mode]
 
     def reduce(self, mode: int, out: torch.Tensor, stream=None):
         """K2 of the owned super-shards (after the post-K1 barrier)."""
