@@ -213,6 +213,7 @@ def build_tile_plans(st: DeviceShardedTensor, rank: int) -> bool:
     val_p = lambda t: t.data_ptr() if t is not None else None
     plans = []
     ok = True
+    failure = None
     for n in range(nmodes):
         w = works[n]
         a, b = st.active, 1 - st.active
@@ -230,8 +231,9 @@ def build_tile_plans(st: DeviceShardedTensor, rank: int) -> bool:
                 bins.data_ptr(), strm)
             if rc == _lib.ERR_UNSUPPORTED:
                 ok = False
-            elif rc != 0:
-                raise _lib.FlycooError(
+            elif rc != 0:  # raised after the walk has brought the tensor back to mode 0
+                ok = False
+                failure = _lib.FlycooError(
                     f"fc_tile_plan_emit failed ({rc}): {L.fc_last_error().decode(errors='replace')}")
             else:
                 plans.append((perm, bins))
@@ -243,6 +245,8 @@ def build_tile_plans(st: DeviceShardedTensor, rank: int) -> bool:
         st._expected += st.nnz
         st.swap((n + 1) % nmodes, still_canonical=True)
     check_errors(st)
+    if failure is not None:
+        raise failure
     if ok:
         for w, (perm, bins) in zip(works, plans):
             w.tile_perm, w.tile_bins = perm, bins
